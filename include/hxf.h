@@ -1,0 +1,154 @@
+/* hxf — C-ABI of the B200-native BP1-BP6 operator + PCG path.
+ *
+ * The drop-in boundary for the reference's (hexfem) operator API.  Plain
+ * pointers and sizes only; every entry point returns an int status
+ * (HXF_OK = 0) and leaves a thread-local message in hxf_last_error().  The
+ * error classes map one to one onto the reference's exception types:
+ *   HXF_EINVAL   <-> std::invalid_argument  (shape/size/parameter errors)
+ *   HXF_ENUMERIC <-> std::runtime_error     (NaN, indefinite, det J <= 0)
+ * (see proj/src/operator.cpp:26-46,67-68, pcg.cpp:27-31,54,75-91,
+ *  qfunction.cpp:82-89,120 under /root/reference).
+ *
+ * Memory-space argument: HXF_HOST pointers are staged through pinned buffers
+ * (functional parity with the reference's host-span signatures);
+ * HXF_DEVICE pointers are used in place (the performance path).
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns HXF_ECUDA. */
+#ifndef HXF_H
+#define HXF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HXF_ABI_VERSION 1
+
+typedef enum {
+  HXF_OK = 0,
+  HXF_EINVAL = 1,      /* std::invalid_argument */
+  HXF_ENUMERIC = 2,    /* std::runtime_error (numerical failure) */
+  HXF_ECUDA = 3,       /* CUDA runtime failure / no device */
+  HXF_ENCCL = 4,       /* collective failure */
+  HXF_EUNSUPPORTED = 5 /* (p, q, m) combination without a compiled kernel */
+} hxf_status;
+
+typedef enum { HXF_HOST = 0, HXF_DEVICE = 1 } hxf_memspace;
+typedef enum { HXF_INTERP = 0, HXF_GRAD = 1 } hxf_eval_mode;          /* EvalMode */
+typedef enum { HXF_FORWARD = 0, HXF_TRANSPOSE = 1 } hxf_eval_dir;      /* EvalDirection */
+typedef enum { HXF_QDATA_MASS = 0, HXF_QDATA_DIFFUSION = 1 } hxf_qdata_kind; /* QDataKind */
+
+typedef struct hxf_ctx hxf_ctx;
+typedef struct hxf_op hxf_op;
+
+/* Thread-local description of the last failure on this thread. */
+const char* hxf_last_error(void);
+int hxf_abi_version(void);
+/* Number of hxf kernels launched so far in this process (instrumentation). */
+int64_t hxf_launch_count(void);
+
+/* ---- context: one CUDA device (+ optional NCCL communicator) ----------- */
+int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out);
+int hxf_context_destroy(hxf_ctx* ctx);
+/* cudaStream_t the context launches on (as void*). */
+void* hxf_context_stream(hxf_ctx* ctx);
+
+/* ---- operator: replaces make_operator + MatFreeOperator --------------------
+ * proj/include/hexfem/operator.hpp:19-38 (make_operator), validation as in
+ * proj/src/operator.cpp:20-62.  Arrays are copied to the device at creation;
+ * the handle is immutable afterwards. */
+typedef struct {
+  int p;                     /* basis degree (TensorBasis::p) */
+  int q;                     /* 1-D quadrature points (TensorBasis::q) */
+  int m;                     /* components (ElemRestriction::m) */
+  int64_t num_elements;      /* ElemRestriction::num_elements */
+  int64_t n_L;               /* ElemRestriction::n_L (scalar nodes) */
+  const double* interp1d;    /* q x (p+1) row-major, TensorBasis::interp1d */
+  const double* grad1d;      /* q x (p+1) row-major, TensorBasis::grad1d */
+  const double* qpoints;     /* q quadrature points on [-1,1] (TensorBasis::quad.points) */
+  const int64_t* indices;    /* num_elements x (p+1)^3, ElemRestriction::indices; NULL =
+                                structured box given by dims (mesh.cpp:80-104 numbering) */
+  int dims[3];               /* structured-box hint (elements per axis) or {0,0,0} */
+  const double* mass_qdata;  /* E*q^3 (QData Mass values) or NULL */
+  const double* diff_qdata;  /* E*6*q^3 (QData Diffusion values) or NULL */
+  hxf_memspace qdata_space;  /* where the two qdata arrays live */
+  double alpha, beta;        /* y = (alpha A + beta B) x */
+  const int64_t* constrained;/* scalar L-indices (any order, duplicates allowed) */
+  int64_t n_constrained;
+  int block;                 /* KernelPlan::block — accepted and ignored */
+} hxf_operator_desc;
+
+int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* desc, hxf_op** out);
+int hxf_operator_destroy(hxf_op* op);
+/* size = m * n_L (MatFreeOperator::size) */
+int64_t hxf_operator_size(const hxf_op* op);
+/* 1 when the index table was recognised as the structured box and G/G^T are
+ * computed from the lattice (no index traffic), 0 for the int32 table path. */
+int hxf_operator_is_structured(const hxf_op* op);
+
+/* operator_apply (operator.hpp:53-58, operator.cpp:64-144): y is overwritten;
+ * constrained entries satisfy y = x.  stream: cudaStream_t or NULL for the
+ * context stream.  Synchronous for HXF_HOST, stream-ordered for HXF_DEVICE. */
+int hxf_operator_apply(hxf_op* op, const double* x, double* y, hxf_memspace space, void* stream);
+
+/* operator_diagonal (operator.hpp:60-64, operator.cpp:170-256). */
+int hxf_operator_diagonal(hxf_op* op, double* d, hxf_memspace space);
+
+/* apply_g / apply_g_transpose over the operator's restriction
+ * (restriction.hpp:35-42): E-vector layout e[(c*E+e)*S + s]. */
+int hxf_restriction_apply(hxf_op* op, int transpose, const double* in, double* out,
+                          hxf_memspace space);
+/* multiplicity (restriction.hpp:44-45): n_L doubles. */
+int hxf_restriction_multiplicity(hxf_op* op, double* out, hxf_memspace space);
+
+/* apply_basis_batch (contraction.hpp:56-67, contraction.cpp:248-332) for ne
+ * single-component element blocks; Grad data component-outermost across the
+ * batch, (d*ne + e)*q^3.  Output overwritten. */
+int hxf_basis_apply(hxf_ctx* ctx, int p, int q, const double* interp1d, const double* grad1d,
+                    hxf_eval_mode mode, hxf_eval_dir dir, int64_t ne, const double* in,
+                    double* out, hxf_memspace space);
+
+/* apply_qf_mass / apply_qf_diffusion (qfunction.hpp:33-43) for elements
+ * [e0, e0+ne) of a QData array of num_elements x (1|6) x nq values. */
+int hxf_qfunction_apply(hxf_ctx* ctx, hxf_qdata_kind kind, const double* qdata,
+                        int64_t num_elements, int nq, int64_t e0, int64_t ne, const double* in,
+                        double* out, hxf_memspace space);
+
+/* compute_qdata (qfunction.hpp:27-31, qfunction.cpp:12-122) on the device:
+ * coords = 3*n_L component-major node coordinates, indices = E x (p+1)^3
+ * (or NULL with dims set for the structured box), qweights = q 1-D weights.
+ * out = E*(1|6)*q^3.  HXF_ENUMERIC when det J <= 0 (message names the
+ * element and quadrature point). */
+int hxf_qdata_compute(hxf_ctx* ctx, int p, int q, const double* interp1d, const double* grad1d,
+                      const double* qweights, int64_t num_elements, int64_t n_L,
+                      const double* coords, const int64_t* indices, const int dims[3],
+                      hxf_qdata_kind kind, double* out, hxf_memspace space);
+
+/* ---- PCG: replaces pcg(ApplyFn, ...) for this operator ---------------------
+ * proj/include/hexfem/pcg.hpp:13-41, proj/src/pcg.cpp:24-115.  x0 = 0;
+ * diag = NULL means unpreconditioned.  Runs device-resident: only b (and the
+ * diagonal) go in, x and the report come out. */
+typedef struct {
+  double tol_rel;       /* PcgOptions::tol_rel */
+  int max_iter;         /* PcgOptions::max_iter */
+  int fixed_iterations; /* PcgOptions::fixed_iterations, < 0 = unset */
+} hxf_pcg_options;
+
+typedef struct {
+  int iterations;            /* SolveReport::iterations */
+  int converged;             /* SolveReport::converged */
+  double* residual_history;  /* caller buffer, >= history_capacity entries; entry 0 = ||b|| */
+  int history_capacity;
+  double apply_time_seconds; /* device time inside the operator kernel (CUDA events) */
+  double total_time_seconds; /* device time of the whole solve (CUDA events) */
+} hxf_solve_report;
+
+int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_options* opts,
+            double* x, hxf_memspace space, hxf_solve_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HXF_H */

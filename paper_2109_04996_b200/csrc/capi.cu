@@ -1,0 +1,820 @@
+// The hxf C-ABI (include/hxf.h): context, operator handle, apply, diagonal,
+// restriction / basis / QFunction / geometric-factor entry points and the
+// device-resident PCG driver.
+//
+// Errors are raised internally as HxfError and mapped to the C status codes
+// at the boundary, with the reference's own messages where one exists
+// (proj/src/operator.cpp:26-46,67-68, pcg.cpp:27-31,54,75-91,
+// qfunction.cpp:82-89,120).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "aux_kernels.h"
+#include "hxf_internal.h"
+#include "pcg_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+int g_sms = 0;
+
+struct HxfError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw HxfError{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HXF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HXF_OK;
+  } catch (const HxfError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HXF_ECUDA;
+  }
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+struct DevVec {
+  double* p = nullptr;
+  size_t n = 0;
+  double* ensure(size_t want) {
+    if (want > n) {
+      if (p) cudaFree(p);
+      p = dalloc<double>(want);
+      n = want;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpy H2D");
+}
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpy D2H");
+}
+
+// Lagrange derivative matrix on the q quadrature points (barycentric form,
+// evaluated in long double): D[i][j] = l_j'(x_i).  Used for the collocated-
+// gradient factorisation of interpolating bases (op_kernel.cuh).
+std::vector<double> quad_derivative_matrix(const double* x, int q) {
+  std::vector<long double> w(q, 1.0L);
+  for (int j = 0; j < q; ++j)
+    for (int k = 0; k < q; ++k)
+      if (k != j) w[j] *= (long double)x[j] - (long double)x[k];
+  std::vector<double> D(size_t(q) * q, 0.0);
+  for (int i = 0; i < q; ++i) {
+    long double diag = 0.0L;
+    for (int j = 0; j < q; ++j) {
+      if (j == i) continue;
+      const long double v = (w[i] / w[j]) / ((long double)x[i] - (long double)x[j]);
+      D[size_t(i) * q + j] = (double)v;
+      diag -= v;
+    }
+    D[size_t(i) * q + i] = (double)diag;
+  }
+  return D;
+}
+
+}  // namespace
+
+namespace hxf {
+
+int num_sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+int max_op_grid() { return num_sms() * 32; }
+
+cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams& prm,
+                      const double* B, const double* D, cudaStream_t s, int* grid_out) {
+  switch (P) {
+#define HXF_CASE(N) \
+  case N:           \
+    return launch_op_p##N(Q, NC, interp, qk, prm, B, D, s, grid_out);
+    HXF_CASE(2) HXF_CASE(3) HXF_CASE(4) HXF_CASE(5) HXF_CASE(6) HXF_CASE(7) HXF_CASE(8)
+    HXF_CASE(9) HXF_CASE(10) HXF_CASE(11) HXF_CASE(12) HXF_CASE(13) HXF_CASE(14) HXF_CASE(15)
+    HXF_CASE(16)
+#undef HXF_CASE
+    default:
+      return cudaErrorNotSupported;
+  }
+}
+
+}  // namespace hxf
+
+using namespace hxf;
+
+struct hxf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* nccl = nullptr;
+  DevVec scratch_a, scratch_b, scratch_c, scratch_d;  // API-surface staging
+};
+
+struct hxf_op {
+  hxf_ctx* ctx = nullptr;
+  int p = 0, q = 0, m = 1, P = 0, Q = 0;
+  int64_t E = 0, n_L = 0;
+  bool interp = false;
+  std::vector<double> B, Dq;  // kernel-parameter matrices
+  double alpha = 0, beta = 0;
+  bool structured = false;
+  int nx = 0, ny = 0, nz = 0;
+  int64_t NX = 0, NY = 0, NZ = 0;
+  int* d_idx = nullptr;
+  int cons_mode = 0;
+  uint32_t* d_mask = nullptr;
+  int64_t ncons = 0;
+  double* d_qd_diff = nullptr;
+  int64_t diff_stride = 0;
+  double* d_qd_mass = nullptr;
+  int64_t mass_stride = 0;
+  double* d_part = nullptr;
+  double *d_B = nullptr, *d_G = nullptr, *d_Bt = nullptr, *d_Gt = nullptr;
+  double *d_bb = nullptr, *d_dd = nullptr, *d_bd = nullptr;
+  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_vpart, w_hist, w_ediag, w_ldiag;
+  PcgState* d_state = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+
+  int64_t size() const { return int64_t(m) * n_L; }
+  Lattice lattice() const {
+    Lattice L;
+    L.p = p;
+    L.S = (p + 1) * (p + 1) * (p + 1);
+    L.E = E;
+    L.n_L = n_L;
+    L.NX = NX;
+    L.NY = NY;
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    return L;
+  }
+  ~hxf_op() {
+    for (void* ptr : {(void*)d_idx, (void*)d_mask, (void*)d_qd_diff, (void*)d_qd_mass,
+                      (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
+                      (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state})
+      if (ptr) cudaFree(ptr);
+    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_vpart, &w_hist, &w_ediag,
+                      &w_ldiag})
+      v->release();
+    for (auto e : ev) cudaEventDestroy(e);
+    if (ev_t0) cudaEventDestroy(ev_t0);
+    if (ev_t1) cudaEventDestroy(ev_t1);
+  }
+};
+
+namespace {
+
+cudaStream_t pick_stream(hxf_op* op, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : op->ctx->stream;
+}
+
+// y = op x on the device (y zeroed here; the kernel REDs into it).
+// dot_part: per-CTA partials of x_free . y (fused p.Ap), *nparts set.
+void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
+                  int* nparts, const int* stop, bool zero_y = true) {
+  if (zero_y) ck(cudaMemsetAsync(y, 0, sizeof(double) * op->size(), s), "cudaMemsetAsync");
+  OpParams prm{};
+  prm.x = x;
+  prm.y = y;
+  prm.E = op->E;
+  prm.n_L = op->n_L;
+  prm.NX = op->NX;
+  prm.NY = op->NY;
+  prm.NZ = op->NZ;
+  prm.nx = op->nx;
+  prm.ny = op->ny;
+  prm.idx = op->structured ? nullptr : op->d_idx;
+  prm.cons_mode = op->cons_mode;
+  prm.cons_mask = op->d_mask;
+  prm.stop = stop;
+  int total = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const double coef = pass == 0 ? op->alpha : op->beta;
+    if (coef == 0.0) continue;
+    prm.qd = pass == 0 ? op->d_qd_diff : op->d_qd_mass;
+    prm.coef = coef;
+    prm.dot_partials = dot_part ? dot_part + total : nullptr;
+    int grid = 0;
+    const cudaError_t err = launch_op(op->P, op->Q, op->m, op->interp, pass == 0 ? 1 : 2, prm,
+                                      op->B.data(), op->Dq.data(), s, &grid);
+    if (err == cudaErrorNotSupported)
+      fail(HXF_EUNSUPPORTED, "operator kernel not instantiated for this (p, q, m)");
+    ck(err, "operator kernel launch");
+    total += grid;
+  }
+  if (nparts) *nparts = total;
+}
+
+std::vector<int64_t> sorted_unique(const int64_t* v, int64_t n) {
+  std::vector<int64_t> out(v, v + n);
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+
+// Recognise the reference's structured-box numbering (mesh.cpp:80-104) and
+// verify it entry by entry (bit-exact assembly map).
+bool detect_structured(hxf_op* op, const int64_t* idx, const int dims[3]) {
+  const int p = op->p, n1 = p + 1;
+  const int64_t S = int64_t(n1) * n1 * n1;
+  int64_t nx = dims ? dims[0] : 0, ny = dims ? dims[1] : 0, nz = dims ? dims[2] : 0;
+  if (!idx) {  // implicit structured box (dims validated by the caller)
+    const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
+    if (nx * ny * nz != op->E || NX * NY * NZ != op->n_L)
+      fail(HXF_EINVAL, "make_operator: dims do not match num_elements / n_L");
+    op->nx = int(nx);
+    op->ny = int(ny);
+    op->nz = int(nz);
+    op->NX = NX;
+    op->NY = NY;
+    op->NZ = NZ;
+    return true;
+  }
+  if (nx <= 0 || ny <= 0 || nz <= 0) {
+    const int64_t NXg = idx[n1];           // node of slot (0,1,0) in element 0
+    const int64_t NXNY = idx[n1 * n1];     // node of slot (0,0,1)
+    if (NXg <= 1 || (NXg - 1) % p || NXNY % NXg) return false;
+    nx = (NXg - 1) / p;
+    const int64_t NYg = NXNY / NXg;
+    if ((NYg - 1) % p) return false;
+    ny = (NYg - 1) / p;
+    if (nx * ny == 0 || op->E % (nx * ny)) return false;
+    nz = op->E / (nx * ny);
+  }
+  if (nx * ny * nz != op->E) return false;
+  const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
+  if (NX * NY * NZ != op->n_L) return false;
+  for (int64_t e = 0; e < op->E; ++e) {
+    const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
+    const int64_t* row = idx + e * S;
+    int64_t s = 0;
+    for (int kz = 0; kz <= p; ++kz)
+      for (int ky = 0; ky <= p; ++ky)
+        for (int kx = 0; kx <= p; ++kx, ++s)
+          if (row[s] != (ex * p + kx) + NX * ((ey * p + ky) + NY * (ez * p + kz))) return false;
+  }
+  op->nx = int(nx);
+  op->ny = int(ny);
+  op->nz = int(nz);
+  op->NX = NX;
+  op->NY = NY;
+  op->NZ = NZ;
+  return true;
+}
+
+void upload_qdata(hxf_op* op, const double* src, int nplanes, hxf_memspace space, double** dst,
+                  int64_t* stride) {
+  const int64_t Q3 = int64_t(op->q) * op->q * op->q;
+  const int64_t w = nplanes * Q3;
+  *stride = (w + 1) / 2 * 2;  // 16-byte element blocks for the bulk copy
+  *dst = dalloc<double>(size_t(op->E) * *stride + 2);
+  ck(cudaMemcpy2DAsync(*dst, size_t(*stride) * 8, src, size_t(w) * 8, size_t(w) * 8,
+                       size_t(op->E),
+                       space == HXF_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       op->ctx->stream),
+     "qdata upload");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hxf_last_error(void) { return g_err.c_str(); }
+int hxf_abi_version(void) { return HXF_ABI_VERSION; }
+int64_t hxf_launch_count(void) { return g_launches.load(); }
+
+int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(HXF_EINVAL, "hxf_context_create: out is NULL");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      fail(HXF_ECUDA, "hxf: no CUDA device (there is no CPU fallback)");
+    if (device < 0 || device >= n) fail(HXF_EINVAL, "hxf_context_create: bad device ordinal");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      fail(HXF_ECUDA, "hxf kernels are compiled for sm_100a (B200); device is sm_" +
+                          std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* c = new hxf_ctx();
+    c->device = device;
+    c->nccl = nccl_comm;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    g_sms = prop.multiProcessorCount;
+    *out = c;
+  });
+}
+
+int hxf_context_destroy(hxf_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (DevVec* v : {&ctx->scratch_a, &ctx->scratch_b, &ctx->scratch_c, &ctx->scratch_d})
+      v->release();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* hxf_context_stream(hxf_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* d, hxf_op** out) {
+  return guarded([&] {
+    if (!ctx || !d || !out) fail(HXF_EINVAL, "hxf_operator_create: NULL argument");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (d->alpha < 0 || d->beta < 0 || (d->alpha == 0 && d->beta == 0))
+      fail(HXF_EINVAL, "make_operator: alpha, beta must be >= 0 and not both zero");
+    if (d->p < 1 || d->q < 1 || d->m < 1 || d->num_elements < 1 || d->n_L < 1)
+      fail(HXF_EINVAL, "make_operator: restriction/basis size mismatch");
+    if (!d->interp1d || !d->grad1d)
+      fail(HXF_EINVAL, "make_operator: basis tables are required");
+    if (!d->indices && (d->dims[0] < 1 || d->dims[1] < 1 || d->dims[2] < 1))
+      fail(HXF_EINVAL, "make_operator: indices (or structured-box dims) are required");
+    if (d->beta > 0 && !d->mass_qdata) fail(HXF_EINVAL, "make_operator: mass qdata required");
+    if (d->alpha > 0 && !d->diff_qdata)
+      fail(HXF_EINVAL, "make_operator: diffusion qdata required");
+    auto op = std::make_unique<hxf_op>();
+    op->ctx = ctx;
+    op->p = d->p;
+    op->q = d->q;
+    op->m = d->m;
+    op->P = d->p + 1;
+    op->Q = d->q;
+    op->E = d->num_elements;
+    op->n_L = d->n_L;
+    op->alpha = d->alpha;
+    op->beta = d->beta;
+    const int n1 = d->p + 1, q = d->q;
+    const int64_t S = int64_t(n1) * n1 * n1;
+    if (op->P > 16) fail(HXF_EUNSUPPORTED, "hxf: p > 15 has no compiled kernel");
+    if (d->indices)
+      for (int64_t i = 0; i < op->E * S; ++i)
+        if (d->indices[i] < 0 || d->indices[i] >= d->n_L)
+          fail(HXF_EINVAL, "make_operator: restriction index out of range");
+    std::vector<int64_t> cons;
+    if (d->n_constrained > 0) {
+      if (!d->constrained) fail(HXF_EINVAL, "make_operator: constrained list is NULL");
+      cons = sorted_unique(d->constrained, d->n_constrained);
+      if (cons.front() < 0 || cons.back() >= d->n_L)
+        fail(HXF_EINVAL, "make_operator: constrained index out of range");
+    }
+    // basis: collocated (interp1d == I exactly) or interpolating with q = p+2
+    bool ident = q == n1;
+    for (int i = 0; ident && i < q; ++i)
+      for (int j = 0; j < n1; ++j)
+        if (d->interp1d[i * n1 + j] != (i == j ? 1.0 : 0.0)) {
+          ident = false;
+          break;
+        }
+    op->B.assign(d->interp1d, d->interp1d + size_t(q) * n1);
+    if (ident) {
+      op->interp = false;
+      op->Dq.assign(d->grad1d, d->grad1d + size_t(q) * n1);
+    } else if (q == n1 + 1) {
+      if (!d->qpoints) fail(HXF_EINVAL, "make_operator: quadrature points required (q != p+1)");
+      op->interp = true;
+      op->Dq = quad_derivative_matrix(d->qpoints, q);
+    } else {
+      fail(HXF_EUNSUPPORTED, "hxf: basis needs q = p+1 collocated GLL or q = p+2");
+    }
+    // restriction: structured lattice or int32 table
+    op->structured = detect_structured(op.get(), d->indices, d->dims);
+    if (!op->structured) {
+      if (d->n_L >= (int64_t(1) << 31)) fail(HXF_EUNSUPPORTED, "hxf: n_L >= 2^31 with a table");
+      std::vector<int> idx32(size_t(op->E * S));
+      for (size_t i = 0; i < idx32.size(); ++i) idx32[i] = int(d->indices[i]);
+      op->d_idx = dalloc<int>(idx32.size());
+      ck(cudaMemcpy(op->d_idx, idx32.data(), idx32.size() * sizeof(int), cudaMemcpyHostToDevice),
+         "index upload");
+    }
+    // constraints: box boundary (computed in the kernel) or bitmask
+    op->ncons = int64_t(cons.size());
+    if (!cons.empty()) {
+      std::vector<uint32_t> mask(size_t((d->n_L + 31) / 32), 0u);
+      for (int64_t c : cons) mask[size_t(c >> 5)] |= 1u << (c & 31);
+      op->d_mask = dalloc<uint32_t>(mask.size());
+      ck(cudaMemcpy(op->d_mask, mask.data(), mask.size() * 4, cudaMemcpyHostToDevice),
+         "mask upload");
+      op->cons_mode = 2;
+      if (op->structured) {
+        const int64_t nb = op->n_L - (op->NX - 2) * (op->NY - 2) * (op->NZ - 2);
+        bool boundary = int64_t(cons.size()) == nb && op->NX > 1 && op->NY > 1 && op->NZ > 1;
+        for (size_t i = 0; boundary && i < cons.size(); ++i) {
+          const int64_t c = cons[i], ix = c % op->NX, iy = (c / op->NX) % op->NY,
+                        iz = c / (op->NX * op->NY);
+          boundary = ix == 0 || ix == op->NX - 1 || iy == 0 || iy == op->NY - 1 || iz == 0 ||
+                     iz == op->NZ - 1;
+        }
+        if (boundary) op->cons_mode = 1;
+      }
+    }
+    if (op->alpha > 0) upload_qdata(op.get(), d->diff_qdata, 6, d->qdata_space, &op->d_qd_diff,
+                                    &op->diff_stride);
+    if (op->beta > 0) upload_qdata(op.get(), d->mass_qdata, 1, d->qdata_space, &op->d_qd_mass,
+                                   &op->mass_stride);
+    op->d_part = dalloc<double>(size_t(2 * max_op_grid()));
+    // 1-D tables for the setup / API-surface kernels
+    std::vector<double> Bt(size_t(q) * n1), Gt(size_t(q) * n1), bb(Bt.size()), dd(Bt.size()),
+        bd(Bt.size());
+    for (int iq = 0; iq < q; ++iq)
+      for (int j = 0; j < n1; ++j) {
+        Bt[size_t(j) * q + iq] = d->interp1d[iq * n1 + j];
+        Gt[size_t(j) * q + iq] = d->grad1d[iq * n1 + j];
+      }
+    for (size_t i = 0; i < Bt.size(); ++i) {
+      bb[i] = Bt[i] * Bt[i];
+      dd[i] = Gt[i] * Gt[i];
+      bd[i] = Bt[i] * Gt[i];
+    }
+    auto up = [&](const double* src, size_t n) {
+      double* p = dalloc<double>(n);
+      ck(cudaMemcpy(p, src, n * 8, cudaMemcpyHostToDevice), "table upload");
+      return p;
+    };
+    op->d_B = up(d->interp1d, Bt.size());
+    op->d_G = up(d->grad1d, Bt.size());
+    op->d_Bt = up(Bt.data(), Bt.size());
+    op->d_Gt = up(Gt.data(), Bt.size());
+    op->d_bb = up(bb.data(), Bt.size());
+    op->d_dd = up(dd.data(), Bt.size());
+    op->d_bd = up(bd.data(), Bt.size());
+    ck(cudaStreamSynchronize(ctx->stream), "operator create");
+    *out = op.release();
+  });
+}
+
+int hxf_operator_destroy(hxf_op* op) {
+  return guarded([&] {
+    if (!op) return;
+    cudaStreamSynchronize(op->ctx->stream);
+    delete op;
+  });
+}
+
+int64_t hxf_operator_size(const hxf_op* op) { return op ? op->size() : 0; }
+int hxf_operator_is_structured(const hxf_op* op) { return op && op->structured ? 1 : 0; }
+
+int hxf_operator_apply(hxf_op* op, const double* x, double* y, hxf_memspace space, void* stream) {
+  return guarded([&] {
+    if (!op || !x || !y) fail(HXF_EINVAL, "operator_apply: shape mismatch");
+    cudaStream_t s = pick_stream(op, stream);
+    const size_t n = size_t(op->size());
+    if (space == HXF_DEVICE) {
+      device_apply(op, x, y, s, nullptr, nullptr, nullptr);
+      ck(cudaGetLastError(), "operator_apply");
+      return;
+    }
+    double* dx = op->w_x.ensure(n);
+    double* dy = op->w_y.ensure(n);
+    h2d(dx, x, n * 8, s);
+    device_apply(op, dx, dy, s, nullptr, nullptr, nullptr);
+    d2h(y, dy, n * 8, s);
+    ck(cudaStreamSynchronize(s), "operator_apply");
+  });
+}
+
+int hxf_operator_diagonal(hxf_op* op, double* d, hxf_memspace space) {
+  return guarded([&] {
+    if (!op || !d) fail(HXF_EINVAL, "operator_diagonal: NULL argument");
+    cudaStream_t s = op->ctx->stream;
+    const Lattice L = op->lattice();
+    double* ediag = op->w_ediag.ensure(size_t(op->E) * L.S);
+    double* ldiag = op->w_ldiag.ensure(size_t(op->n_L));
+    double* dd = space == HXF_DEVICE ? d : op->w_y.ensure(size_t(op->size()));
+    ck(launch_diagonal(s, L, op->structured ? nullptr : op->d_idx, op->structured, op->q, op->d_bb,
+                       op->d_dd, op->d_bd, op->d_qd_mass, op->mass_stride, op->d_qd_diff,
+                       op->diff_stride, op->alpha, op->beta, op->m, op->d_mask, ediag, ldiag, dd),
+       "operator_diagonal");
+    if (space == HXF_HOST) d2h(d, dd, size_t(op->size()) * 8, s);
+    ck(cudaStreamSynchronize(s), "operator_diagonal");
+  });
+}
+
+int hxf_restriction_apply(hxf_op* op, int transpose, const double* in, double* out,
+                          hxf_memspace space) {
+  return guarded([&] {
+    if (!op || !in || !out) fail(HXF_EINVAL, "apply_g: NULL argument");
+    cudaStream_t s = op->ctx->stream;
+    const Lattice L = op->lattice();
+    const size_t nl = size_t(op->m) * op->n_L, ne = size_t(op->m) * op->E * L.S;
+    const size_t nin = transpose ? ne : nl, nout = transpose ? nl : ne;
+    const double* din = in;
+    double* dout = out;
+    if (space == HXF_HOST) {
+      double* a = op->ctx->scratch_a.ensure(nin);
+      h2d(a, in, nin * 8, s);
+      din = a;
+      dout = op->ctx->scratch_b.ensure(nout);
+    }
+    ck(launch_restriction(s, L, op->structured ? nullptr : op->d_idx, op->structured, op->m,
+                          transpose != 0, din, dout),
+       "restriction");
+    if (space == HXF_HOST) d2h(out, dout, nout * 8, s);
+    ck(cudaStreamSynchronize(s), "restriction");
+  });
+}
+
+int hxf_restriction_multiplicity(hxf_op* op, double* out, hxf_memspace space) {
+  return guarded([&] {
+    if (!op || !out) fail(HXF_EINVAL, "multiplicity: NULL argument");
+    cudaStream_t s = op->ctx->stream;
+    double* dout = space == HXF_DEVICE ? out : op->ctx->scratch_b.ensure(size_t(op->n_L));
+    ck(launch_multiplicity(s, op->lattice(), op->structured ? nullptr : op->d_idx, dout),
+       "multiplicity");
+    if (space == HXF_HOST) d2h(out, dout, size_t(op->n_L) * 8, s);
+    ck(cudaStreamSynchronize(s), "multiplicity");
+  });
+}
+
+int hxf_basis_apply(hxf_ctx* ctx, int p, int q, const double* interp1d, const double* grad1d,
+                    hxf_eval_mode mode, hxf_eval_dir dir, int64_t ne, const double* in,
+                    double* out, hxf_memspace space) {
+  return guarded([&] {
+    if (!ctx || !interp1d || !grad1d || !in || !out)
+      fail(HXF_EINVAL, "apply_basis_batch: NULL argument");
+    if (p < 1 || q < 1 || p > 16 || q > 17) fail(HXF_EINVAL, "apply_basis_batch: bad p/q");
+    cudaStream_t s = ctx->stream;
+    const int n1 = p + 1;
+    const size_t msz = size_t(q) * n1;
+    std::vector<double> tabs(4 * msz);
+    std::memcpy(tabs.data(), interp1d, msz * 8);
+    std::memcpy(tabs.data() + msz, grad1d, msz * 8);
+    for (int iq = 0; iq < q; ++iq)
+      for (int j = 0; j < n1; ++j) {
+        tabs[2 * msz + size_t(j) * q + iq] = interp1d[iq * n1 + j];
+        tabs[3 * msz + size_t(j) * q + iq] = grad1d[iq * n1 + j];
+      }
+    double* dt = ctx->scratch_c.ensure(tabs.size());
+    h2d(dt, tabs.data(), tabs.size() * 8, s);
+    const int64_t nd3 = int64_t(n1) * n1 * n1, nq3 = int64_t(q) * q * q;
+    const int64_t in_e = (mode == HXF_GRAD && dir == HXF_TRANSPOSE) ? 3 * nq3
+                         : (dir == HXF_FORWARD ? nd3 : nq3);
+    const int64_t out_e = (mode == HXF_GRAD && dir == HXF_FORWARD) ? 3 * nq3
+                          : (dir == HXF_FORWARD ? nq3 : nd3);
+    const double* din = in;
+    double* dout = out;
+    if (space == HXF_HOST) {
+      double* a = ctx->scratch_a.ensure(size_t(ne * in_e));
+      h2d(a, in, size_t(ne * in_e) * 8, s);
+      din = a;
+      dout = ctx->scratch_b.ensure(size_t(ne * out_e));
+    }
+    ck(launch_basis_apply(s, p, q, dt, dt + msz, dt + 2 * msz, dt + 3 * msz, int(mode), int(dir),
+                          ne, din, dout),
+       "apply_basis_batch");
+    if (space == HXF_HOST) d2h(out, dout, size_t(ne * out_e) * 8, s);
+    ck(cudaStreamSynchronize(s), "apply_basis_batch");
+  });
+}
+
+int hxf_qfunction_apply(hxf_ctx* ctx, hxf_qdata_kind kind, const double* qdata,
+                        int64_t num_elements, int nq, int64_t e0, int64_t ne, const double* in,
+                        double* out, hxf_memspace space) {
+  return guarded([&] {
+    if (!ctx || !qdata || !in || !out) fail(HXF_EINVAL, "apply_qf: NULL argument");
+    if (e0 < 0 || ne < 0 || e0 + ne > num_elements)
+      fail(HXF_EINVAL, kind == HXF_QDATA_MASS ? "apply_qf_mass: shape mismatch"
+                                              : "apply_qf_diffusion: shape mismatch");
+    cudaStream_t s = ctx->stream;
+    const int K = kind == HXF_QDATA_MASS ? 1 : 3;
+    const int Kq = kind == HXF_QDATA_MASS ? 1 : 6;
+    const size_t nio = size_t(K) * ne * nq;
+    const double* dq = qdata;
+    const double* din = in;
+    double* dout = out;
+    int64_t ebase = e0;
+    if (space == HXF_HOST) {
+      double* q = ctx->scratch_c.ensure(size_t(Kq) * ne * nq);
+      h2d(q, qdata + size_t(e0) * Kq * nq, size_t(Kq) * ne * nq * 8, s);
+      dq = q;
+      ebase = 0;
+      double* a = ctx->scratch_a.ensure(nio);
+      h2d(a, in, nio * 8, s);
+      din = a;
+      dout = ctx->scratch_b.ensure(nio);
+    }
+    ck(launch_qfunction(s, kind == HXF_QDATA_MASS ? 0 : 1, dq, nq, ebase, ne, din, dout),
+       "apply_qf");
+    if (space == HXF_HOST) d2h(out, dout, nio * 8, s);
+    ck(cudaStreamSynchronize(s), "apply_qf");
+  });
+}
+
+int hxf_qdata_compute(hxf_ctx* ctx, int p, int q, const double* interp1d, const double* grad1d,
+                      const double* qweights, int64_t num_elements, int64_t n_L,
+                      const double* coords, const int64_t* indices, const int dims[3],
+                      hxf_qdata_kind kind, double* out, hxf_memspace space) {
+  return guarded([&] {
+    if (!ctx || !interp1d || !grad1d || !qweights || !coords || !out)
+      fail(HXF_EINVAL, "compute_qdata: NULL argument");
+    if (p < 1 || q < 1 || p > 16 || q > 17) fail(HXF_EINVAL, "compute_qdata: bad p/q");
+    cudaStream_t s = ctx->stream;
+    const int n1 = p + 1;
+    const int64_t S = int64_t(n1) * n1 * n1, nq = int64_t(q) * q * q;
+    Lattice L{};
+    L.p = p;
+    L.S = int(S);
+    L.E = num_elements;
+    L.n_L = n_L;
+    int* d_idx = nullptr;
+    if (indices) {
+      std::vector<int> idx32(size_t(num_elements * S));
+      for (size_t i = 0; i < idx32.size(); ++i) idx32[i] = int(indices[i]);
+      d_idx = dalloc<int>(idx32.size());
+      h2d(d_idx, idx32.data(), idx32.size() * 4, s);
+    } else {
+      if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 ||
+          int64_t(dims[0]) * dims[1] * dims[2] != num_elements)
+        fail(HXF_EINVAL, "compute_qdata: dims required without an index table");
+      L.nx = dims[0];
+      L.ny = dims[1];
+      L.nz = dims[2];
+      L.NX = int64_t(dims[0]) * p + 1;
+      L.NY = int64_t(dims[1]) * p + 1;
+    }
+    const size_t msz = size_t(q) * n1;
+    std::vector<double> tabs(2 * msz + size_t(q));
+    std::memcpy(tabs.data(), interp1d, msz * 8);
+    std::memcpy(tabs.data() + msz, grad1d, msz * 8);
+    std::memcpy(tabs.data() + 2 * msz, qweights, size_t(q) * 8);
+    double* dt = ctx->scratch_c.ensure(tabs.size());
+    h2d(dt, tabs.data(), tabs.size() * 8, s);
+    const double* dcoords = coords;
+    if (space == HXF_HOST) {
+      double* c = ctx->scratch_a.ensure(size_t(3 * n_L));
+      h2d(c, coords, size_t(3 * n_L) * 8, s);
+      dcoords = c;
+    }
+    const int K = kind == HXF_QDATA_MASS ? 1 : 6;
+    double* dout = space == HXF_DEVICE ? out : ctx->scratch_b.ensure(size_t(num_elements * K * nq));
+    const int64_t batch = std::max<int64_t>(1, (int64_t(256) << 20) / (9 * nq * 8));
+    double* scratch = ctx->scratch_d.ensure(size_t(9 * std::min(batch, num_elements) * nq));
+    unsigned long long* fkey = dalloc<unsigned long long>(1);
+    double* fdet = dalloc<double>(1);
+    const unsigned long long init = ~0ull;
+    h2d(fkey, &init, 8, s);
+    ck(launch_qdata(s, L, d_idx, q, dt, dt + msz, dt + 2 * msz, dcoords, kind == HXF_QDATA_MASS ? 0 : 1,
+                    dout, scratch, std::min(batch, num_elements), fkey, fdet),
+       "compute_qdata");
+    unsigned long long key = 0;
+    double det = 0;
+    d2h(&key, fkey, 8, s);
+    d2h(&det, fdet, 8, s);
+    if (space == HXF_HOST) d2h(out, dout, size_t(num_elements * K * nq) * 8, s);
+    ck(cudaStreamSynchronize(s), "compute_qdata");
+    cudaFree(fkey);
+    cudaFree(fdet);
+    if (d_idx) cudaFree(d_idx);
+    if (key != ~0ull) {
+      char buf[256];
+      std::snprintf(buf, sizeof buf,
+                    "compute_qdata: non-positive Jacobian determinant (%f) in element %lld at "
+                    "quadrature point %lld",
+                    det, (long long)(key / nq), (long long)(key % nq));
+      fail(HXF_ENUMERIC, buf);
+    }
+  });
+}
+
+int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_options* opts,
+            double* x, hxf_memspace space, hxf_solve_report* report) {
+  return guarded([&] {
+    if (!op || !b || !x || !opts || !report) fail(HXF_EINVAL, "pcg: vector length mismatch");
+    cudaStream_t s = op->ctx->stream;
+    const size_t n = size_t(op->size());
+    const bool fixed = opts->fixed_iterations >= 0;
+    const int limit = fixed ? opts->fixed_iterations : opts->max_iter;
+    if (limit < 0) fail(HXF_EINVAL, "pcg: negative iteration limit");
+    if (!op->d_state) op->d_state = dalloc<PcgState>(1);
+    if (!op->ev_t0) {
+      ck(cudaEventCreate(&op->ev_t0), "event");
+      ck(cudaEventCreate(&op->ev_t1), "event");
+    }
+    while (op->ev.size() < size_t(2 * limit)) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "event");
+      op->ev.push_back(e);
+    }
+    // operands
+    const double *db = b, *dd = diag;
+    double* dx = x;
+    if (space == HXF_HOST) {
+      double* tb = op->w_b.ensure(n);
+      h2d(tb, b, n * 8, s);
+      db = tb;
+      if (diag) {
+        double* td = op->w_d.ensure(n);
+        h2d(td, diag, n * 8, s);
+        dd = td;
+      }
+      dx = op->w_x.ensure(n);
+    }
+    double* r = op->w_r.ensure(n);
+    double* p = op->w_p.ensure(n);
+    double* Ap = op->w_Ap.ensure(n);
+    double* vpart = op->w_vpart.ensure(size_t(3 * vec_grid()));
+    double* hist = op->w_hist.ensure(size_t(limit) + 2);
+    PcgState st{};
+    st.tol = opts->tol_rel;
+    st.limit = limit;
+    st.fixed = fixed ? 1 : 0;
+    ck(cudaEventRecord(op->ev_t0, s), "event");
+    h2d(op->d_state, &st, sizeof st, s);
+    ck(pcg_launch_init(s, op->n_L, op->m, db, dd, dx, r, p, Ap, op->d_mask, vpart, op->d_state, hist),
+       "pcg init");
+    const int* stop = &op->d_state->stop;
+    int launched = 0;
+    PcgState hs{};
+    ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
+    ck(cudaStreamSynchronize(s), "pcg init");
+    if (hs.stop && hs.error) launched = limit;  // fall through to the error report
+    while (!hs.stop && launched < limit) {
+      const int chunk = fixed ? limit : std::min(limit - launched, launched < 4 ? 1 : 8);
+      for (int i = 0; i < chunk; ++i, ++launched) {
+        int nparts = 0;
+        ck(cudaEventRecord(op->ev[2 * launched], s), "event");
+        // Ap was zeroed by the init / direction kernel: no memset pass here
+        device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false);
+        ck(cudaEventRecord(op->ev[2 * launched + 1], s), "event");
+        ck(pcg_launch_alpha(s, op->d_state, op->d_part, nparts), "pcg alpha");
+        ck(pcg_launch_update(s, op->d_state, int64_t(n), dd, dx, r, p, Ap, vpart, hist),
+           "pcg update");
+        ck(pcg_launch_direction(s, op->d_state, op->n_L, op->m, dd, r, p, Ap, op->d_mask, vpart),
+           "pcg direction");
+      }
+      ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
+      ck(cudaStreamSynchronize(s), "pcg");
+    }
+    ck(cudaEventRecord(op->ev_t1, s), "event");
+    ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
+    if (space == HXF_HOST) d2h(x, dx, n * 8, s);
+    ck(cudaStreamSynchronize(s), "pcg");
+    if (hs.error) {
+      static const char* msgs[] = {"", "pcg: right-hand side is not finite",
+                                   "pcg: NaN in operator apply",
+                                   "pcg: indefinite direction (p^T A p <= 0), operator is not SPD",
+                                   "pcg: residual is not finite"};
+      fail(HXF_ENUMERIC, msgs[hs.error]);
+    }
+    const int iters = hs.it;
+    report->iterations = iters;
+    report->converged = (hs.converged || hs.res <= hs.target) ? 1 : 0;
+    if (report->residual_history && report->history_capacity > 0) {
+      const int nh = std::min(report->history_capacity, iters + 1);
+      ck(cudaMemcpy(report->residual_history, hist, size_t(nh) * 8, cudaMemcpyDeviceToHost),
+         "history");
+    }
+    double apply_ms = 0;
+    for (int i = 0; i < std::min(iters, launched); ++i) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, op->ev[2 * i], op->ev[2 * i + 1]), "elapsed");
+      apply_ms += ms;
+    }
+    float tot = 0;
+    ck(cudaEventElapsedTime(&tot, op->ev_t0, op->ev_t1), "elapsed");
+    report->apply_time_seconds = apply_ms * 1e-3;
+    report->total_time_seconds = tot * 1e-3;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal declarations shared by the hxf CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hxf.h"
+
+namespace hxf {
+
+// Arguments of the fused operator kernel (op_kernel.cuh).
+struct OpParams {
+  const double* x;
+  double* y;
+  const double* qd;          // per-element padded geometric factors
+  int64_t E, n_L;            // elements, scalar nodes (component stride)
+  int64_t NX, NY, NZ;        // structured-box lattice
+  int nx, ny;                // elements per axis (x, y)
+  const int* idx;            // int32 E x P^3 table, or nullptr (structured box)
+  int cons_mode;             // 0 none, 1 box boundary, 2 bitmask
+  const uint32_t* cons_mask; // n_L bits (mode 2)
+  double* dot_partials;      // per-CTA partial of x_masked . y, or nullptr
+  const int* stop;           // device flag: skip the whole kernel when set (PCG)
+  double coef;               // alpha (diffusion) or beta (mass)
+};
+
+// Launch the fused operator kernel instance for (P, Q, NC, interp, qk);
+// returns cudaErrorNotSupported for an uninstantiated combination.
+// B: q x p1 row-major interp1d, D: q x q derivative at the quadrature points.
+cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams& prm,
+                      const double* B, const double* D, cudaStream_t s, int* grid_out);
+
+// Upper bound on the grid of any launch_op() call (partials buffer size).
+int max_op_grid();
+
+// Per-P launchers (op_inst_p*.cu)
+#define HXF_DECL_P(N)                                                                          \
+  cudaError_t launch_op_p##N(int Q, int NC, bool interp, int qk, const OpParams& prm,       \
+                             const double* B, const double* D, cudaStream_t s, int* grid_out);
+HXF_DECL_P(2)
+HXF_DECL_P(3)
+HXF_DECL_P(4)
+HXF_DECL_P(5)
+HXF_DECL_P(6)
+HXF_DECL_P(7)
+HXF_DECL_P(8)
+HXF_DECL_P(9)
+HXF_DECL_P(10)
+HXF_DECL_P(11)
+HXF_DECL_P(12)
+HXF_DECL_P(13)
+HXF_DECL_P(14)
+HXF_DECL_P(15)
+HXF_DECL_P(16)
+#undef HXF_DECL_P
+
+int num_sms();
+void count_launch(int n = 1);
+
+}  // namespace hxf

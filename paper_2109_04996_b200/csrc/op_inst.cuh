@@ -1,0 +1,69 @@
+// Instantiates the fused operator kernel for one degree P = p+1 (included by
+// op_inst_p<P>.cu with HXF_P defined, so the instances compile in parallel).
+#include <cstring>
+
+#include "op_kernel.cuh"
+
+namespace hxf {
+namespace {
+
+template <int P, int Q, int NC, bool INTERP, int QK>
+struct Pick {
+  // stream the geometric factors through shared memory (bulk copy, double
+  // buffered) whenever that still leaves room for two CTAs per SM
+  static constexpr bool QSMEM = OpTraits<P, Q, NC, INTERP, QK, true>::SMEM_BYTES <= 112 * 1024;
+  using T = OpTraits<P, Q, NC, INTERP, QK, QSMEM>;
+};
+
+template <class T>
+cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStream_t s,
+                int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_apply_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  OpMats<T::P, T::Q> mats;
+  std::memset(&mats, 0, sizeof mats);
+  if (T::INTERP) std::memcpy(mats.B, B, sizeof(double) * T::Q * T::P);
+  std::memcpy(mats.D, D, sizeof(double) * T::Q * T::Q);
+  const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
+  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int P, int Q, bool INTERP>
+cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const double* D,
+                  cudaStream_t s, int* g) {
+  if (NC == 1 && qk == 1) return run<typename Pick<P, Q, 1, INTERP, 1>::T>(prm, B, D, s, g);
+  if (NC == 1 && qk == 2) return run<typename Pick<P, Q, 1, INTERP, 2>::T>(prm, B, D, s, g);
+  if (NC == 3 && qk == 1) return run<typename Pick<P, Q, 3, INTERP, 1>::T>(prm, B, D, s, g);
+  if (NC == 3 && qk == 2) return run<typename Pick<P, Q, 3, INTERP, 2>::T>(prm, B, D, s, g);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace
+
+#define HXF_CAT2(a, b) a##b
+#define HXF_CAT(a, b) HXF_CAT2(a, b)
+cudaError_t HXF_CAT(launch_op_p, HXF_P)(int Q, int NC, bool interp, int qk, const OpParams& prm,
+                                       const double* B, const double* D, cudaStream_t s,
+                                       int* grid_out) {
+  constexpr int P = HXF_P;
+  if (!interp && Q == P) return run_q<P, P, false>(NC, qk, prm, B, D, s, grid_out);
+  if (interp && Q == P + 1) return run_q<P, P + 1, true>(NC, qk, prm, B, D, s, grid_out);
+  return cudaErrorNotSupported;
+}
+
+}  // namespace hxf

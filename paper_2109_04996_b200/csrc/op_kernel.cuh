@@ -1,0 +1,411 @@
+// K1: the fused BP operator kernel  y = G^T B^T D B G x  (one launch per apply).
+//
+// Replaces, in one kernel, the reference's five materialising passes
+// (proj/src/operator.cpp:64-144): mask + apply_g (restriction.cpp:28-48),
+// apply_basis_batch forward (contraction.cpp:248-295), apply_qf_mass /
+// apply_qf_diffusion (qfunction.cpp:124-162), apply_basis_batch transpose,
+// and the colour-ordered apply_g_transpose (restriction.cpp:50-75) + axpy.
+//
+// Layout / execution (B200-first):
+//   * persistent CTAs, each owning element steps b, b+G, b+2G, ... so the
+//     whole grid sweeps the lexicographic element order as one wavefront and
+//     x/y lines shared by neighbouring elements are reused from L2;
+//   * per step, EPB elements; one thread per (qi,qj) quadrature column, the
+//     z-line of the column lives in registers (z contractions with the 1-D
+//     matrices as kernel-parameter constant operands), x/y contractions go
+//     through a shared-memory slab;
+//   * the geometric factors of the NEXT step stream into shared memory with a
+//     single bulk async copy (TMA engine, L2 evict_first) tracked by an
+//     mbarrier, double-buffered, while the current step computes;
+//   * G is computed from the structured-box lattice (or an int32 table for a
+//     general mesh); G^T is an FP64 RED into y (zeroed by the caller), and
+//     constrained nodes are written y = x directly (operator.cpp:141-143);
+//   * optionally, the partial p.(Ap) over unconstrained nodes is reduced per
+//     CTA (the first PCG dot, pcg.cpp:74, fused).
+//
+// Interpolating bases (BP1-4, q != p+1 or Gauss points) use the collocated-
+// gradient factorisation: u_q = (B x B x B) u, grad = D_q u_q with D_q the
+// derivative matrix of the Lagrange basis on the q quadrature points.  It is
+// exact for degree-p polynomials (D_q B = G), so it matches the reference's
+// B,G chains (contraction.cpp:279-293) to rounding.
+#pragma once
+#include "hxf_device.cuh"
+#include "hxf_internal.h"
+
+namespace hxf {
+
+__host__ __device__ constexpr int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+template <int Q>
+struct EpbChoice {
+  // elements per CTA step: fill 64..192 threads, cap the per-step qdata slab
+  static constexpr int QQ = Q * Q;
+  static constexpr int value = QQ >= 64 ? 1 : (QQ == 25 ? 5 : (QQ == 36 ? 5 : (QQ == 49 ? 3 : 64 / QQ)));
+};
+
+template <int P_, int Q_, int NC_, bool INTERP_, int QK_, bool QSMEM_>
+struct OpTraits {
+  static constexpr int P = P_, Q = Q_, NC = NC_, QK = QK_;
+  static constexpr bool INTERP = INTERP_, QSMEM = QSMEM_;
+  static constexpr bool DIFF = (QK & 1) != 0, MASS = (QK & 2) != 0;
+  static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
+  static constexpr int EPB = EpbChoice<Q>::value;
+  static constexpr int NT = round_up(EPB * QQ, 32);
+  static constexpr int NQD = (DIFF ? 6 : 0) + (MASS ? 1 : 0);
+  static constexpr int QDS = round_up(NQD * Q3, 2);  // padded doubles per element (16 B)
+  static constexpr bool INPLACE = (NC == 1) && DIFF && QSMEM;
+  static constexpr int SP = P | 1, SQ = Q | 1;  // odd strides: conflict-free column reads
+  // shared-memory carve-up (doubles)
+  static constexpr int OFF_B = 0;                          // [Q][SP]  B[qi][a]
+  static constexpr int OFF_BT = OFF_B + (INTERP ? Q * SP : 0);   // [P][SQ]  B[a][i]
+  static constexpr int OFF_D = OFF_BT + (INTERP ? P * SQ : 0);   // [Q][SQ]  D[qi][a]
+  static constexpr int OFF_DT = OFF_D + (DIFF ? Q * SQ : 0);     // [Q][SQ]  D[a][qi]
+  static constexpr int OFF_QD = round_up(OFF_DT + (DIFF ? Q * SQ : 0), 2);
+  static constexpr int QD_STAGE = EPB * QDS;
+  static constexpr int OFF_A = OFF_QD + (QSMEM ? 2 * QD_STAGE : 0);  // EPB x Q^3
+  static constexpr int OFF_BF = OFF_A + EPB * Q3;                     // EPB x P^2 Q
+  static constexpr int OFF_V = OFF_BF + (INTERP ? EPB * P * P * Q : 0);  // EPB x 2 Q^3
+  static constexpr int SMEM_DOUBLES = OFF_V + ((DIFF && !INPLACE) ? EPB * 2 * Q3 : 0);
+  static constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
+};
+
+template <int P, int Q>
+struct OpMats {
+  double B[Q * P];  // interp1d, q x (p+1) row-major (unused when collocated)
+  double D[Q * Q];  // derivative at the quadrature points (= grad1d when collocated)
+};
+
+template <class T>
+__global__ void __launch_bounds__(T::NT)
+    op_apply_kernel(const OpParams prm, const OpMats<T::P, T::Q> mats) {
+  constexpr int P = T::P, Q = T::Q, NC = T::NC, QQ = T::QQ, Q3 = T::Q3;
+  constexpr int EPB = T::EPB, NT = T::NT, SP = T::SP, SQ = T::SQ;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t qbar[2];
+  __shared__ double red_scratch[NT / 32 + 1];
+
+  if (prm.stop && *prm.stop) return;  // PCG already stopped: uniform early exit
+  const int tid = threadIdx.x;
+  const int slot = tid / QQ;
+  const int lt = tid - slot * QQ;
+  const int qi = lt % Q, qj = lt / Q;
+  const bool active_slot = slot < EPB;
+
+  double* sB = smem + T::OFF_B;
+  double* sBT = smem + T::OFF_BT;
+  double* sD = smem + T::OFF_D;
+  double* sDT = smem + T::OFF_DT;
+  double* sQD = smem + T::OFF_QD;
+  double* A = smem + T::OFF_A + (active_slot ? slot : 0) * Q3;
+  double* Bf = smem + T::OFF_BF + (active_slot ? slot : 0) * (P * P * Q);
+  double* Vbuf = smem + T::OFF_V + (active_slot ? slot : 0) * 2 * Q3;
+
+  // 1-D matrices into padded shared memory (thread-varying row index).
+  for (int t = tid; t < Q * Q; t += NT) {
+    const int r = t / Q, c = t % Q;
+    if constexpr (T::DIFF) {
+      sD[r * SQ + c] = mats.D[r * Q + c];
+      sDT[c * SQ + r] = mats.D[r * Q + c];
+    }
+  }
+  if constexpr (T::INTERP) {
+    for (int t = tid; t < Q * P; t += NT) {
+      const int r = t / P, c = t % P;  // B[r][c], r < Q, c < P
+      sB[r * SP + c] = mats.B[t];
+      sBT[c * SQ + r] = mats.B[t];
+    }
+  }
+
+  const int64_t nsteps = (prm.E + EPB - 1) / EPB;
+  const int64_t G = gridDim.x;
+  uint64_t policy = 0;
+  if constexpr (T::QSMEM) {
+    if (tid == 0) {
+      mbar_init(&qbar[0], 1);
+      mbar_init(&qbar[1], 1);
+      fence_mbar_init();
+      policy = l2_evict_first_policy();
+      const int64_t s0 = blockIdx.x;
+      if (s0 < nsteps) {
+        const int64_t e0 = s0 * EPB;
+        const int ne = (int)((prm.E - e0) < EPB ? (prm.E - e0) : EPB);
+        const uint32_t bytes = (uint32_t)(ne * T::QDS * 8);
+        mbar_arrive_expect_tx(&qbar[0], bytes);
+        bulk_g2s(sQD, prm.qd + e0 * T::QDS, bytes, &qbar[0], policy);
+      }
+    }
+  }
+  __syncthreads();
+
+  double dot_acc = 0.0;
+  int it = 0;
+  for (int64_t step = blockIdx.x; step < nsteps; step += G, ++it) {
+    const int stage = it & 1;
+    const int64_t e = step * EPB + slot;
+    const bool active = active_slot && e < prm.E;
+    const double* qd_slot;
+    if constexpr (T::QSMEM) {
+      // prefetch the next step's geometric factors into the other stage
+      if (tid == 0) {
+        const int64_t ns = step + G;
+        if (ns < nsteps) {
+          const int64_t e0 = ns * EPB;
+          const int ne = (int)((prm.E - e0) < EPB ? (prm.E - e0) : EPB);
+          const uint32_t bytes = (uint32_t)(ne * T::QDS * 8);
+          mbar_arrive_expect_tx(&qbar[stage ^ 1], bytes);
+          bulk_g2s(sQD + (stage ^ 1) * T::QD_STAGE, prm.qd + e0 * T::QDS, bytes, &qbar[stage ^ 1],
+                   policy);
+        }
+      }
+      qd_slot = sQD + stage * T::QD_STAGE + (active_slot ? slot : 0) * T::QDS;
+    } else {
+      qd_slot = prm.qd + (active ? e : 0) * T::QDS;
+    }
+
+    // element lattice origin (structured box) for G / G^T
+    int64_t ex = 0, ey = 0, ez = 0;
+    if (active && !prm.idx) {
+      ex = e % prm.nx;
+      const int64_t r = e / prm.nx;
+      ey = r % prm.ny;
+      ez = r / prm.ny;
+    }
+    auto node_of = [&](int i, int j, int k, bool& cons) -> int64_t {
+      int64_t node;
+      if (prm.idx) {
+        node = prm.idx[e * (P * P * P) + i + P * (j + P * k)];
+        cons = prm.cons_mode == 2 && ((prm.cons_mask[node >> 5] >> (node & 31)) & 1u);
+      } else {
+        const int64_t ix = ex * (P - 1) + i, iy = ey * (P - 1) + j, iz = ez * (P - 1) + k;
+        node = ix + prm.NX * (iy + prm.NY * iz);
+        if (prm.cons_mode == 1)
+          cons = ix == 0 || ix == prm.NX - 1 || iy == 0 || iy == prm.NY - 1 || iz == 0 ||
+                 iz == prm.NZ - 1;
+        else if (prm.cons_mode == 2)
+          cons = (prm.cons_mask[node >> 5] >> (node & 31)) & 1u;
+        else
+          cons = false;
+      }
+      return node;
+    };
+
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      const double* xc = prm.x + c * prm.n_L;
+      double* yc = prm.y + c * prm.n_L;
+      if (c > 0) __syncthreads();  // A / V reuse across components
+
+      // ---- G: gather the masked input column (i,j) = (qi,qj) ----
+      double u[P];
+      const bool gthread = active && qi < P && qj < P;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        u[k] = 0.0;
+        if (gthread) {
+          bool cons;
+          const int64_t node = node_of(qi, qj, k, cons);
+          u[k] = cons ? 0.0 : __ldg(xc + node);
+        }
+      }
+
+      double uq[Q];
+      if constexpr (!T::INTERP) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          uq[k] = u[k];
+          if (active_slot) A[k * QQ + qj * Q + qi] = uq[k];
+        }
+        __syncthreads();
+      } else {
+        // x: [P][P][P] -> Bf [P][P][Q]
+        if (gthread) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) A[k * P * P + qj * P + qi] = u[k];
+        }
+        __syncthreads();
+        if (active_slot && qj < P) {
+          double t[P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) t[k] = 0.0;
+#pragma unroll
+          for (int a = 0; a < P; ++a) {
+            const double b = sB[qi * SP + a];
+#pragma unroll
+            for (int k = 0; k < P; ++k) t[k] += b * A[k * P * P + qj * P + a];
+          }
+#pragma unroll
+          for (int k = 0; k < P; ++k) Bf[k * P * Q + qj * Q + qi] = t[k];
+        }
+        __syncthreads();
+        // y: Bf -> registers r[P] at (qi,qj); z: registers -> uq[Q]
+        double r[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) r[k] = 0.0;
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+          const double bb = sB[qj * SP + b];
+#pragma unroll
+          for (int k = 0; k < P; ++k) r[k] += bb * Bf[k * P * Q + b * Q + qi];
+        }
+#pragma unroll
+        for (int kq = 0; kq < Q; ++kq) {
+          double s = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < P; ++cc) s += mats.B[kq * P + cc] * r[cc];
+          uq[kq] = s;
+        }
+        if (active_slot) {
+#pragma unroll
+          for (int kq = 0; kq < Q; ++kq) A[kq * QQ + qj * Q + qi] = uq[kq];
+        }
+        __syncthreads();
+      }
+
+      if constexpr (T::QSMEM) {
+        if (c == 0) mbar_wait(&qbar[stage], (uint32_t)((it >> 1) & 1));
+      }
+
+      // ---- D: derivatives at the quadrature points + pointwise QFunction ----
+      double w[Q];
+      double v2[Q];
+      double* V0 = T::INPLACE ? const_cast<double*>(qd_slot) : Vbuf;
+      double* V1 = T::INPLACE ? const_cast<double*>(qd_slot) + Q3 : Vbuf + Q3;
+      if constexpr (T::DIFF) {
+        double g0[Q], g1[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) g0[k] = g1[k] = 0.0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          const double d0 = sD[qi * SQ + a], d1 = sD[qj * SQ + a];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            g0[k] += d0 * A[k * QQ + qj * Q + a];
+            g1[k] += d1 * A[k * QQ + a * Q + qi];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          double g2 = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < Q; ++cc) g2 += mats.D[k * Q + cc] * uq[cc];
+          const int pt = k * QQ + qj * Q + qi;
+          double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
+          if (active) {
+            s00 = qd_slot[0 * Q3 + pt];
+            s01 = qd_slot[1 * Q3 + pt];
+            s02 = qd_slot[2 * Q3 + pt];
+            s11 = qd_slot[3 * Q3 + pt];
+            s12 = qd_slot[4 * Q3 + pt];
+            s22 = qd_slot[5 * Q3 + pt];
+          }
+          const double v0 = s00 * g0[k] + s01 * g1[k] + s02 * g2;
+          const double v1 = s01 * g0[k] + s11 * g1[k] + s12 * g2;
+          v2[k] = s02 * g0[k] + s12 * g1[k] + s22 * g2;
+          if (active_slot) {
+            V0[pt] = v0;
+            V1[pt] = v1;
+          }
+          w[k] = 0.0;
+          if constexpr (T::MASS) {
+            const double m = active ? qd_slot[6 * Q3 + pt] : 0.0;
+            w[k] = m * uq[k];
+          }
+        }
+        __syncthreads();
+        // transposed derivative
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+          const double t0 = sDT[qi * SQ + a], t1 = sDT[qj * SQ + a];
+#pragma unroll
+          for (int k = 0; k < Q; ++k)
+            w[k] += t0 * V0[k * QQ + qj * Q + a] + t1 * V1[k * QQ + a * Q + qi];
+        }
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int cc = 0; cc < Q; ++cc) s += mats.D[cc * Q + k] * v2[cc];
+          w[k] += s;
+        }
+      } else {
+        // mass only
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const int pt = k * QQ + qj * Q + qi;
+          const double m = active ? qd_slot[pt] : 0.0;
+          w[k] = m * uq[k];
+        }
+      }
+
+      // ---- B^T (interpolating bases) ----
+      double yv[P];
+      if constexpr (!T::INTERP) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) yv[k] = w[k];
+      } else {
+        // z^T: registers -> A as [P][Q][Q]
+        if (active_slot) {
+#pragma unroll
+          for (int cc = 0; cc < P; ++cc) {
+            double s = 0.0;
+#pragma unroll
+            for (int kq = 0; kq < Q; ++kq) s += mats.B[kq * P + cc] * w[kq];
+            A[cc * QQ + qj * Q + qi] = s;
+          }
+        }
+        __syncthreads();
+        // y^T: A [P][Q][Q] -> Bf [P][P][Q]
+        if (active_slot && qj < P) {
+          double t[P];
+#pragma unroll
+          for (int cc = 0; cc < P; ++cc) t[cc] = 0.0;
+#pragma unroll
+          for (int b = 0; b < Q; ++b) {
+            const double bt = sBT[qj * SQ + b];
+#pragma unroll
+            for (int cc = 0; cc < P; ++cc) t[cc] += bt * A[cc * QQ + b * Q + qi];
+          }
+#pragma unroll
+          for (int cc = 0; cc < P; ++cc) Bf[cc * P * Q + qj * Q + qi] = t[cc];
+        }
+        __syncthreads();
+        // x^T: Bf -> yv[P] at (qi,qj), qi,qj < P
+#pragma unroll
+        for (int cc = 0; cc < P; ++cc) yv[cc] = 0.0;
+        if (gthread) {
+#pragma unroll
+          for (int a = 0; a < Q; ++a) {
+            const double bt = sBT[qi * SQ + a];
+#pragma unroll
+            for (int cc = 0; cc < P; ++cc) yv[cc] += bt * Bf[cc * P * Q + qj * Q + a];
+          }
+        }
+      }
+
+      // ---- G^T: RED into y; constrained nodes get y = x ----
+      if (gthread) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          bool cons;
+          const int64_t node = node_of(qi, qj, k, cons);
+          if (cons) {
+            yc[node] = __ldg(xc + node);
+          } else {
+            const double yk = prm.coef * yv[k];  // y += coef * (...)  (operator.cpp:131-135)
+            red_add(yc + node, yk);
+            dot_acc += u[k] * yk;
+          }
+        }
+      }
+    }
+    if constexpr (T::QSMEM) fence_proxy_async_smem();
+    __syncthreads();  // stage buffer and slabs free for reuse
+  }
+
+  if (prm.dot_partials) {
+    const double s = block_sum<NT>(dot_acc, red_scratch);
+    if (tid == 0) prm.dot_partials[blockIdx.x] = s;
+  }
+}
+
+}  // namespace hxf

@@ -1,0 +1,27 @@
+// Device-resident PCG state and launchers (pcg_kernels.cu).
+#pragma once
+#include "hxf_internal.h"
+
+namespace hxf {
+
+enum PcgError { PCG_OK = 0, PCG_ERR_RHS = 1, PCG_ERR_APPLY_NAN = 2, PCG_ERR_INDEFINITE = 3,
+                PCG_ERR_RESID = 4 };
+
+struct PcgState {
+  double rho, pap, alpha, beta, norm_b, target, res, tol, cons_pp;
+  int it, stop, converged, error, limit, fixed;
+};
+
+int vec_grid();
+cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b, const double* d,
+                            double* x, double* r, double* p, double* Ap, const uint32_t* mask,
+                            double* part, PcgState* st, double* hist);
+cudaError_t pcg_launch_alpha(cudaStream_t s, PcgState* st, const double* kpart, int gk);
+cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int64_t n, const double* d, double* x,
+                              double* r, const double* p, const double* Ap, double* part,
+                              double* hist);
+cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int64_t n_L, int m,
+                                 const double* d, const double* r, double* p, double* Ap,
+                                 const uint32_t* mask, double* part);
+
+}  // namespace hxf

@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+vectors and the CPU oracle.  Bars (BASELINE.json north_star): restriction
+indices / assembly maps bit-exact; operator apply rel_max_diff <= 1e-12
+(FP64, max|a-b|/max|a|, tests/oracle_helpers.hpp:74-81); CG iterations +-1."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from gpu_common import GOLDEN, op_from_golden, op_from_oracle, qpoints, tables
+from paper_2109_04996_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+APPLY_TOL = 1e-12
+CASES = sorted(p.stem for p in GOLDEN.glob("bp*.npz"))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = capi.Context(0)
+    yield c
+    c.close()
+
+
+def load(name):
+    return dict(np.load(GOLDEN / f"{name}.npz"))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_matches_reference_golden(ctx, name):
+    g = load(name)
+    if "qdata_diff" not in g and "qdata_mass" not in g:
+        pytest.skip("fixture without qdata")
+    op = op_from_golden(ctx, g)
+    assert op.structured
+    y = op.apply(g["x"])
+    assert oracle.rel_max_diff(g["y"], y) <= APPLY_TOL
+    # constrained pass-through is exact (operator.cpp:141-143)
+    cons = g["constrained"]
+    m, n_L = int(g["info"][0]), int(g["info"][1])
+    for c in range(m):
+        assert np.array_equal(y[c * n_L + cons], g["x"][c * n_L + cons])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_table_path_matches(ctx, name):
+    """Same operator through the int32 index-table (unstructured) path."""
+    g = load(name)
+    if "qdata_diff" not in g and "qdata_mass" not in g:
+        pytest.skip("fixture without qdata")
+    perm_op = op_from_golden(ctx, g)
+    # scramble the index table so it is not recognised as the box
+    idx = g["indices"].copy().reshape(int(g["info"][2]), -1)
+    bp, p = int(g["bp"]), int(g["p"])
+    m, n_L, E, S, nq, q = (int(v) for v in g["info"][:6])
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(n_L)
+    inv = np.argsort(perm)
+    idx_p = perm[idx].reshape(-1)
+    alpha, beta = (0.0, 1.0) if bp <= 2 else (1.0, 0.0)
+    cons = perm[g["constrained"]] if g["constrained"].size else None
+    op = capi.Operator(ctx, p=p, q=q, m=m, num_elements=E, n_L=n_L, interp1d=g["interp1d"],
+                       grad1d=g["grad1d"], qpoints=qpoints(bp, p), indices=idx_p,
+                       mass_qdata=g.get("qdata_mass") if beta > 0 else None,
+                       diff_qdata=g.get("qdata_diff") if alpha > 0 else None,
+                       alpha=alpha, beta=beta, constrained=cons)
+    assert not op.structured
+    x = g["x"].reshape(m, n_L)
+    xp = np.zeros_like(x)
+    xp[:, perm] = x
+    yp = op.apply(xp.reshape(-1)).reshape(m, n_L)
+    y = yp[:, perm].reshape(-1)
+    assert oracle.rel_max_diff(g["y"], y) <= APPLY_TOL
+    del perm_op, inv
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_diagonal_bitwise(ctx, name):
+    g = load(name)
+    if "qdata_diff" not in g and "qdata_mass" not in g:
+        pytest.skip("fixture without qdata")
+    op = op_from_golden(ctx, g)
+    d = op.diagonal()
+    assert np.array_equal(d, g["diag"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pcg_iterations_and_solution(ctx, name):
+    g = load(name)
+    if "qdata_diff" not in g and "qdata_mass" not in g:
+        pytest.skip("fixture without qdata")
+    op = op_from_golden(ctx, g)
+    diag = g["diag"] if bool(g["jacobi"]) else None
+    x, rep = op.pcg(g["rhs"], diag, tol=float(g["tol"]))
+    assert abs(rep["iterations"] - int(g["iterations"])) <= 1
+    assert rep["converged"] == bool(g["converged"])
+    assert oracle.rel_max_diff(g["solution"], x) <= 1e-8
+    assert abs(rep["residual_history"][0] - g["history"][0]) <= 1e-14 * g["history"][0]
+
+
+def test_restriction_and_multiplicity_bitwise(ctx):
+    g = load("bp6_p3_2x2x1_sine")
+    op = op_from_golden(ctx, g)
+    pr = oracle.setup("bp6", 3, (2, 2, 1), "sine")
+    l = oracle.seeded_uniform(op.size, 3)
+    ev = op.restriction(l)
+    idx = g["indices"].reshape(pr.num_elements, -1)
+    m, n_L = pr.components, pr.num_nodes
+    expect = np.stack([l[c * n_L + idx] for c in range(m)]).reshape(-1)
+    assert np.array_equal(ev, expect)
+    # colour-ordered G^T (restriction.cpp:50-75) in numpy, same order
+    evr = oracle.seeded_uniform(ev.size, 4)
+    got = op.restriction(evr, transpose=True)
+    want = np.zeros(m * n_L)
+    E = pr.num_elements
+    nx, ny, nz = 2, 2, 1
+    for col in range(8):
+        for e in range(E):
+            ex, ey, ez = e % nx, (e // nx) % ny, e // (nx * ny)
+            if (ex & 1) | ((ey & 1) << 1) | ((ez & 1) << 2) != col:
+                continue
+            for c in range(m):
+                for s in range(idx.shape[1]):
+                    want[c * n_L + idx[e, s]] += evr[(c * E + e) * idx.shape[1] + s]
+    assert np.array_equal(got, want)
+    mult = op.multiplicity()
+    assert np.array_equal(mult, np.bincount(idx.ravel(), minlength=n_L).astype(float))
+
+
+def test_basis_apply_bitwise(ctx):
+    t = tables()
+    for p, kind, q in ((3, "gauss", 5), (4, "gll", 5), (2, "gauss", 3)):
+        B, G = oracle.basis(p, kind, q)
+        for mode in ("interp", "grad"):
+            for direction in ("forward", "transpose"):
+                key = f"ab_{p}_{kind}_{q}_{mode}_{direction}"
+                out = ctx.basis_apply(p, q, B, G, mode, direction, 3, t[key + "_in"])
+                assert np.array_equal(out, t[key + "_out"]), key
+
+
+@pytest.mark.parametrize("name", ["bp5_p7_2x2x2_sine", "bp3_p7_2x1x1_sine", "bp2_p2_2x1x3_sine",
+                                  "bp1_p3_2x2x2_none"])
+def test_qdata_compute_bitwise(ctx, name):
+    g = load(name)
+    bp, p = int(g["bp"]), int(g["p"])
+    m, n_L, E, S, nq, q = (int(v) for v in g["info"][:6])
+    kind = "gauss" if bp <= 4 else "gll"
+    _, w = oracle.quadrature(kind, q)
+    for k in ("mass", "diff"):
+        if f"qdata_{k}" not in g:
+            continue
+        for use_idx in (True, False):
+            out = ctx.qdata_compute(p, q, g["interp1d"], g["grad1d"], w, E, n_L, g["coords"],
+                                    indices=g["indices"] if use_idx else None,
+                                    dims=None if use_idx else tuple(int(d) for d in g["dims"]),
+                                    kind="mass" if k == "mass" else "diffusion")
+            assert np.array_equal(out, g[f"qdata_{k}"])
+
+
+def test_qfunction_bitwise(ctx):
+    g = load("bp5_p4_2x2x2_sine")
+    qd = g["qdata_diff"]
+    E, nq = int(g["info"][2]), int(g["info"][4])
+    u = oracle.seeded_uniform(3 * 3 * nq, 8)
+    out = ctx.qfunction_apply("diffusion", qd, E, nq, 2, 3, u)
+    s = qd.reshape(E, 6, nq)[2:5]
+    uu = u.reshape(3, 3, nq)
+    v0 = s[:, 0] * uu[0] + s[:, 1] * uu[1] + s[:, 2] * uu[2]
+    v1 = s[:, 1] * uu[0] + s[:, 3] * uu[1] + s[:, 4] * uu[2]
+    v2 = s[:, 2] * uu[0] + s[:, 4] * uu[1] + s[:, 5] * uu[2]
+    assert np.array_equal(out, np.concatenate([v0.ravel(), v1.ravel(), v2.ravel()]))
+
+
+@pytest.mark.parametrize("bp,p,dims", [("bp5", 7, (5, 4, 3)), ("bp3", 7, (3, 3, 2)),
+                                       ("bp6", 5, (3, 3, 3)), ("bp1", 3, (6, 5, 4)),
+                                       ("bp2", 4, (3, 3, 3)), ("bp4", 2, (4, 4, 4)),
+                                       ("bp5", 1, (7, 6, 5)), ("bp5", 11, (2, 2, 1)),
+                                       ("bp3", 12, (1, 2, 1)), ("bp5", 15, (1, 1, 2))])
+def test_apply_vs_oracle_across_orders(ctx, bp, p, dims):
+    pr = oracle.setup(bp, p, dims, "sine")
+    op = op_from_oracle(ctx, pr)
+    x = oracle.seeded_uniform(pr.size, 99)
+    assert oracle.rel_max_diff(pr.apply(x), op.apply(x)) <= APPLY_TOL
+
+
+def test_device_memspace_and_fused_dot(ctx):
+    import torch
+    pr = oracle.setup("bp5", 7, (4, 4, 4), "sine")
+    op = op_from_oracle(ctx, pr, indices=False)
+    x = oracle.seeded_uniform(pr.size, 64)
+    y_ref = pr.apply(x)
+    xd = torch.from_numpy(x).cuda()
+    torch.cuda.synchronize()
+    yd = op.apply(xd, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert oracle.rel_max_diff(y_ref, yd.cpu().numpy()) <= APPLY_TOL
