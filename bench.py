@@ -1,0 +1,354 @@
+#!/usr/bin/env python3
+"""Benchmark: BP5 GDOF/s (operator apply and per CG iteration) on B200.
+
+Workload (BASELINE.json configs[2]): BP5 collocated Poisson,
+p = 7 (q = 8 GLL), 25^3 elements per GPU = 5,268,024 DOFs, sine-deformed
+box, Jacobi-PCG with the reference RHS b = B f, x0 = 0, 20 fixed iterations
+per step (the reference's bench mode, proj/src/bench.cpp:191-229).
+
+  value    n * 20 / t_step in GDOF/s per CG iteration, device timed (CUDA
+           events on the solver stream), inputs resident in HBM (qdata is
+           384 MB > 126 MB L2, so no L2 flush is needed between steps)
+  apply    GDOF/s of a single operator apply y = A x (memset + fused kernel)
+  e2e      the same CG step through the public API with HOST (pinned)
+           b in / x out: H2D + solve + D2H inside the timed region
+  roofline the fused operator kernel: algorithmic bytes per launch
+           (16 m n_L + 48 E q^3) / its event-timed duration,
+           against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference's own run_bench (oracle/_ref, built from
+           /root/reference sources) on this host's cores, bounded sample
+
+`--impl reference` runs the reference's CPU implementation (oracle/_ref
+`hexfem._core`, the reference's own Python API) on all host cores for the same
+workload and prints the same JSON line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BP5 GDOF/s (operator apply and per CG iter) vs p and DOFs/GPU, 1/2/4/8 B200"
+UNIT = "GDOF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bp", default="bp5")
+    ap.add_argument("--degree", type=int, default=7)
+    ap.add_argument("--elems", type=int, default=25, help="elements per axis per GPU")
+    ap.add_argument("--deform", default="sine")
+    ap.add_argument("--iters", type=int, default=20, help="CG iterations per step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-iters", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def bp_sizes(bp: str, p: int, d: int):
+    m = 1 if int(bp[2]) % 2 == 1 else 3
+    q = p + 2 if int(bp[2]) <= 4 else p + 1
+    n1 = d * p + 1
+    n_L = n1 ** 3
+    cons = int(bp[2]) >= 3
+    n = m * ((n1 - 2) ** 3 if cons else n1 ** 3)
+    E = d ** 3
+    K = 6 if int(bp[2]) >= 3 else 1
+    bytes_apply = 16 * m * n_L + 8 * K * E * q ** 3
+    bytes_cg = bytes_apply + 11 * 8 * m * n_L
+    return dict(m=m, q=q, n_L=n_L, n=n, E=E, bytes_apply=bytes_apply, bytes_cg=bytes_cg)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(ROOT / "MEASURED_PEAKS.json") as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profiled_traffic():
+    """dram bytes per launch of the operator kernel from the committed ncu summary."""
+    try:
+        with open(ROOT / "profiles" / "op_kernel_traffic.json") as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(args, sizes):
+    """The reference's own run_bench on this host's cores (oracle/_ref)."""
+    import oracle
+
+    cores = os.cpu_count() or 1
+    if oracle.available("reference"):
+        t0 = time.perf_counter()
+        rec = oracle.run_bench_reference(args.bp, args.degree, (args.elems,) * 3, cores,
+                                         args.cpu_iters, args.deform)
+        wall = time.perf_counter() - t0
+        return {"value": rec["dofs_rate"] / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": (f"reference run_bench {args.bp} p={args.degree} {args.elems}^3 "
+                           f"{args.deform}, {args.cpu_iters} fixed CG iters, min of 3 reps, "
+                           f"{cores} threads; {wall:.1f}s incl. setup"),
+                "seconds_per_iter": rec["seconds"] / max(rec["iterations"], 1)}
+    # fallback: the C restatement on one core, smaller sample
+    d = max(2, args.elems // 3)
+    pr = oracle.setup(args.bp, args.degree, (d, d, d), args.deform)
+    t0 = time.perf_counter()
+    _, rep = pr.solve(tol=0.0, fixed_iterations=args.cpu_iters)
+    dt = time.perf_counter() - t0
+    return {"value": pr.n * rep["iterations"] / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle port {args.bp} p={args.degree} {d}^3, {args.cpu_iters} CG iters"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    try:
+        import hexfem  # the reference's own Python API, built from its sources
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref not built: {e}"}))
+        return
+    sizes = bp_sizes(args.bp, args.degree, args.elems)
+    prob = hexfem.setup(args.bp, degree=args.degree, dims=(args.elems,) * 3,
+                        deform=args.deform, threads=cores)
+    iters = args.cpu_iters
+    times = []
+    for s in range(args.warmup + args.steps):
+        _, rep = prob.solve(tol=1e-8, fixed_iterations=iters)
+        if s >= args.warmup:
+            times.append(rep["total_time_seconds"])
+    t = sum(times)
+    value = prob.n * iters * len(times) / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (manufactured sin(pi x) sin(pi y) sin(pi z) RHS on the sine-deformed box)",
+        "config": {"workload": f"{args.bp} p={args.degree} {args.elems}^3 {args.deform}, "
+                               f"Jacobi-PCG {iters} fixed iterations per step",
+                   "n_dofs": prob.n, "threads": cores},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"reference Problem.solve, {iters} fixed CG iterations per "
+                                   f"step, PCG timer (pcg.cpp:33-113)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    import paper_2109_04996_b200 as hx
+    from paper_2109_04996_b200 import capi
+
+    sizes = bp_sizes(args.bp, args.degree, args.elems)
+    t_setup = time.perf_counter()
+    prob = hx.setup(args.bp, degree=args.degree, dims=(args.elems,) * 3, deform=args.deform,
+                    device=local)
+    diag_ptr = prob.diag_device_ptr
+    t_setup = time.perf_counter() - t_setup
+    stream = torch.cuda.ExternalStream(prob.stream)
+    n_vec = prob.size
+    x = torch.empty(n_vec, dtype=torch.float64, device=f"cuda:{local}")
+    b_ptr = prob.rhs_device_ptr
+
+    def step():
+        return prob.pcg_device(b_ptr, x.data_ptr(), jacobi=True, tol=1e-8,
+                               fixed_iterations=args.iters)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = capi.launch_count()
+    apply_s = 0.0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = step()
+            apply_s += rep["apply_time_seconds"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = capi.launch_count() - launches0
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * sizes["n"] * args.iters / (ms_step * 1e-3) / 1e9
+    t_k1 = apply_s / (args.steps * args.iters)
+
+    # single operator apply (memset + fused kernel), device timed
+    y = torch.empty_like(x)
+    xin = torch.from_numpy(np.random.default_rng(99).uniform(-1, 1, n_vec)).to(x.device)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        prob.apply_device(xin.data_ptr(), y.data_ptr(), prob.stream)
+    reps = 20
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(reps):
+        prob.apply_device(xin.data_ptr(), y.data_ptr(), prob.stream)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    t_apply = a0.elapsed_time(a1) * 1e-3 / reps
+
+    # e2e: pinned host b in, host x out, through the public API
+    b_host = torch.from_numpy(prob.rhs).pin_memory()
+    x_host = torch.empty(n_vec, dtype=torch.float64).pin_memory()
+    prob.pcg_host(b_host.data_ptr(), x_host.data_ptr(), fixed_iterations=args.iters)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        prob.pcg_host(b_host.data_ptr(), x_host.data_ptr(), fixed_iterations=args.iters)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3) / args.steps
+    e2e_value = world * sizes["n"] * args.iters / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peak()
+    achieved = sizes["bytes_apply"] / t_k1 / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (manufactured sin(pi x) sin(pi y) sin(pi z) RHS on the sine-deformed box)",
+        "config": {"workload": f"{args.bp} p={args.degree} q={sizes['q']} {args.elems}^3 "
+                               f"elements/GPU {args.deform}, Jacobi-PCG {args.iters} fixed "
+                               f"iterations per step",
+                   "n_dofs_per_gpu": sizes["n"], "n_L": sizes["n_L"], "elements": sizes["E"],
+                   "parallelism": f"element partition x{world}" if world > 1 else "single GPU",
+                   "l2_policy": "inputs larger than L2 (qdata 384 MB/GPU > 126 MB)"},
+        "apply": {"gdofs": world * sizes["n"] / t_apply / 1e9, "us": t_apply * 1e6,
+                  "bytes_alg": sizes["bytes_apply"],
+                  "gbs_alg": sizes["bytes_apply"] / t_apply / 1e9},
+        "cg_iter": {"us": ms_step * 1e3 / args.iters, "bytes_alg": sizes["bytes_cg"],
+                    "gbs_alg": sizes["bytes_cg"] / (ms_step * 1e-3 / args.iters) / 1e9,
+                    "operator_kernel_us": t_k1 * 1e6},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": profiled_traffic(),
+                     "kernel": "hxf::op_apply_kernel (fused G^T B^T D B G)",
+                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_vec,
+                "d2h_bytes_per_step": 8 * n_vec},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "setup_seconds": t_setup,
+    }
+    if world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, sizes)
+        except Exception as e:  # report, never fabricate
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -55,6 +55,13 @@ int hxf_context_destroy(hxf_ctx* ctx);
 /* cudaStream_t the context launches on (as void*). */
 void* hxf_context_stream(hxf_ctx* ctx);
 
+/* ---- device memory on the context's device (stream-ordered on its stream) */
+int hxf_malloc(hxf_ctx* ctx, uint64_t bytes, void** out);
+int hxf_free(hxf_ctx* ctx, void* ptr);
+/* kind: 0 host->device, 1 device->host, 2 device->device; synchronous. */
+int hxf_memcpy(hxf_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
+int hxf_synchronize(hxf_ctx* ctx);
+
 /* ---- operator: replaces make_operator + MatFreeOperator --------------------
  * proj/include/hexfem/operator.hpp:19-38 (make_operator), validation as in
  * proj/src/operator.cpp:20-62.  Arrays are copied to the device at creation;

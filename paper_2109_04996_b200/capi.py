@@ -25,6 +25,7 @@ EXPORTS = (
     "hxf_operator_size", "hxf_operator_is_structured", "hxf_operator_apply",
     "hxf_operator_diagonal", "hxf_restriction_apply", "hxf_restriction_multiplicity",
     "hxf_basis_apply", "hxf_qfunction_apply", "hxf_qdata_compute", "hxf_pcg",
+    "hxf_malloc", "hxf_free", "hxf_memcpy", "hxf_synchronize",
 )
 
 

@@ -358,6 +358,43 @@ int hxf_context_destroy(hxf_ctx* ctx) {
 
 void* hxf_context_stream(hxf_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
+int hxf_malloc(hxf_ctx* ctx, uint64_t bytes, void** out) {
+  return guarded([&] {
+    if (!ctx || !out) fail(HXF_EINVAL, "hxf_malloc: NULL argument");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    *out = nullptr;
+    ck(cudaMalloc(out, bytes ? bytes : 1), "cudaMalloc");
+  });
+}
+
+int hxf_free(hxf_ctx* ctx, void* ptr) {
+  return guarded([&] {
+    if (!ctx) fail(HXF_EINVAL, "hxf_free: NULL context");
+    if (ptr) {
+      ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+      ck(cudaFree(ptr), "cudaFree");
+    }
+  });
+}
+
+int hxf_memcpy(hxf_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind) {
+  return guarded([&] {
+    if (!ctx || (!dst && bytes) || (!src && bytes)) fail(HXF_EINVAL, "hxf_memcpy: NULL argument");
+    const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                             : kind == 1 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    ck(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  });
+}
+
+int hxf_synchronize(hxf_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) fail(HXF_EINVAL, "hxf_synchronize: NULL context");
+    ck(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  });
+}
+
 int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* d, hxf_op** out) {
   return guarded([&] {
     if (!ctx || !d || !out) fail(HXF_EINVAL, "hxf_operator_create: NULL argument");

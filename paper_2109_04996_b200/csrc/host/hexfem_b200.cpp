@@ -1,0 +1,538 @@
+// Host-side mirror of the reference BP API over the hxf C-ABI.
+//
+// Setup tables (quadrature, Lagrange basis, mesh lattice, manufactured
+// fields) follow the reference formulas and operation order
+// (proj/src/quadrature.cpp, tensor_basis.cpp, mesh.cpp, bench.cpp) so the
+// node coordinates, restriction numbering and RHS agree with it bit for bit;
+// the geometric factors, operator applies, diagonal and PCG run on the GPU.
+#include "hexfem_b200.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <mutex>
+
+namespace hexfem_b200 {
+
+void check(int status) {
+  if (status == HXF_OK) return;
+  const std::string msg = hxf_last_error();
+  if (status == HXF_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);  // HXF_ENUMERIC and device failures
+}
+
+// ------------------------------------------------------------ quadrature
+namespace {
+struct Legendre {
+  double value, derivative;
+};
+
+Legendre legendre_eval(int n, double x) {
+  if (n == 0) return {1.0, 0.0};
+  double pm1 = 1.0, p = x;
+  for (int k = 1; k < n; ++k) {
+    const double next = ((2 * k + 1) * x * p - k * pm1) / (k + 1);
+    pm1 = p;
+    p = next;
+  }
+  const double denom = x * x - 1.0;
+  const double dp = std::abs(denom) > 1e-10
+                        ? n * (x * p - pm1) / denom
+                        : 0.5 * n * (n + 1) * (x >= 0 ? 1.0 : (n % 2 ? 1.0 : -1.0));
+  return {p, dp};
+}
+}  // namespace
+
+QuadratureRule make_quadrature(QuadratureKind kind, int q) {
+  QuadratureRule r;
+  r.kind = kind;
+  r.q = q;
+  r.points.assign(size_t(std::max(q, 0)), 0.0);
+  r.weights.assign(size_t(std::max(q, 0)), 0.0);
+  if (kind == QuadratureKind::GaussLegendre) {
+    if (q < 1)
+      throw std::invalid_argument("make_quadrature: Gauss-Legendre needs q >= 1, got " +
+                                  std::to_string(q));
+    for (int i = 0; i < q / 2; ++i) {
+      double x = -std::cos(M_PI * (i + 0.75) / (q + 0.5));
+      for (int it = 0; it < 100; ++it) {
+        const Legendre L = legendre_eval(q, x);
+        const double dx = L.value / L.derivative;
+        x -= dx;
+        if (std::abs(dx) <= 1e-15) break;
+      }
+      const double dp = legendre_eval(q, x).derivative;
+      const double w = 2.0 / ((1.0 - x * x) * dp * dp);
+      r.points[size_t(i)] = x;
+      r.weights[size_t(i)] = w;
+      r.points[size_t(q - 1 - i)] = -x;
+      r.weights[size_t(q - 1 - i)] = w;
+    }
+    if (q % 2 == 1) {
+      const double dp = legendre_eval(q, 0.0).derivative;
+      r.points[size_t(q / 2)] = 0.0;
+      r.weights[size_t(q / 2)] = 2.0 / (dp * dp);
+    }
+    return r;
+  }
+  if (q < 2)
+    throw std::invalid_argument("make_quadrature: Gauss-Lobatto-Legendre needs q >= 2, got " +
+                                std::to_string(q));
+  const int n = q - 1;
+  const double end_w = 2.0 / (double(n) * (n + 1));
+  r.points[0] = -1.0;
+  r.points[size_t(q - 1)] = 1.0;
+  r.weights[0] = end_w;
+  r.weights[size_t(q - 1)] = end_w;
+  for (int i = 1; i < q / 2; ++i) {
+    double x = -std::cos(M_PI * i / n);
+    for (int it = 0; it < 100; ++it) {
+      const Legendre L = legendre_eval(n, x);
+      const double d2p = (2.0 * x * L.derivative - double(n) * (n + 1) * L.value) / (1.0 - x * x);
+      const double dx = L.derivative / d2p;
+      x -= dx;
+      if (std::abs(dx) <= 1e-15) break;
+    }
+    const double pv = legendre_eval(n, x).value;
+    const double w = 2.0 / (double(n) * (n + 1) * pv * pv);
+    r.points[size_t(i)] = x;
+    r.weights[size_t(i)] = w;
+    r.points[size_t(q - 1 - i)] = -x;
+    r.weights[size_t(q - 1 - i)] = w;
+  }
+  if (q % 2 == 1) {
+    const double pv = legendre_eval(n, 0.0).value;
+    r.points[size_t(q / 2)] = 0.0;
+    r.weights[size_t(q / 2)] = 2.0 / (double(n) * (n + 1) * pv * pv);
+  }
+  return r;
+}
+
+// ------------------------------------------------------------ basis
+namespace {
+double lagrange(const std::vector<double>& nd, int j, double x) {
+  double r = 1.0;
+  for (int m = 0; m < int(nd.size()); ++m)
+    if (m != j) r *= (x - nd[size_t(m)]) / (nd[size_t(j)] - nd[size_t(m)]);
+  return r;
+}
+double lagrange_d(const std::vector<double>& nd, int j, double x) {
+  double s = 0.0;
+  for (int i = 0; i < int(nd.size()); ++i) {
+    if (i == j) continue;
+    double prod = 1.0;
+    for (int m = 0; m < int(nd.size()); ++m)
+      if (m != i && m != j) prod *= (x - nd[size_t(m)]) / (nd[size_t(j)] - nd[size_t(m)]);
+    s += prod / (nd[size_t(j)] - nd[size_t(i)]);
+  }
+  return s;
+}
+}  // namespace
+
+TensorBasis make_basis(int p, const QuadratureRule& quad) {
+  if (p < 1) throw std::invalid_argument("make_basis: p must be >= 1, got " + std::to_string(p));
+  if (quad.q < 1 || int(quad.points.size()) != quad.q)
+    throw std::invalid_argument("make_basis: invalid quadrature rule");
+  TensorBasis b;
+  b.p = p;
+  b.q = quad.q;
+  b.quad = quad;
+  b.nodes = make_quadrature(QuadratureKind::GaussLobattoLegendre, p + 1).points;
+  b.collocated = quad.kind == QuadratureKind::GaussLobattoLegendre && quad.q == p + 1;
+  const int n1 = p + 1;
+  b.interp1d.assign(size_t(quad.q) * n1, 0.0);
+  b.grad1d.assign(size_t(quad.q) * n1, 0.0);
+  for (int iq = 0; iq < quad.q; ++iq)
+    for (int j = 0; j < n1; ++j) {
+      b.interp1d[size_t(iq) * n1 + j] = lagrange(b.nodes, j, quad.points[size_t(iq)]);
+      b.grad1d[size_t(iq) * n1 + j] = lagrange_d(b.nodes, j, quad.points[size_t(iq)]);
+    }
+  return b;
+}
+
+// ------------------------------------------------------------ mesh
+HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
+  if (nx < 1 || ny < 1 || nz < 1)
+    throw std::invalid_argument("build_mesh: element counts must be >= 1");
+  if (p < 1) throw std::invalid_argument("build_mesh: p must be >= 1");
+  HexMesh mesh;
+  mesh.dims = {nx, ny, nz};
+  mesh.p = p;
+  mesh.deformation = deformation;
+  mesh.nodes_per_axis = {int64_t(nx) * p + 1, int64_t(ny) * p + 1, int64_t(nz) * p + 1};
+  mesh.n_L = mesh.nodes_per_axis[0] * mesh.nodes_per_axis[1] * mesh.nodes_per_axis[2];
+  const std::vector<double> gll = make_quadrature(QuadratureKind::GaussLobattoLegendre, p + 1).points;
+  auto axis = [&](int ne) {
+    std::vector<double> c(size_t(ne) * p + 1);
+    const double h = 1.0 / ne;
+    for (int k = 0; k < ne; ++k)
+      for (int j = 0; j <= p; ++j) c[size_t(k) * p + size_t(j)] = (k + 0.5 * (gll[size_t(j)] + 1.0)) * h;
+    c.back() = 1.0;
+    c.front() = 0.0;
+    return c;
+  };
+  const auto cx = axis(nx), cy = axis(ny), cz = axis(nz);
+  const int64_t NX = mesh.nodes_per_axis[0], NY = mesh.nodes_per_axis[1],
+                NZ = mesh.nodes_per_axis[2];
+  mesh.coords.assign(size_t(3 * mesh.n_L), 0.0);
+  // the sine bump factorises: s(x,y,z) = sin(pi x) sin(pi y) sin(pi z), with
+  // the reference's evaluation order ((eps*sx)*sy)*sz kept per node
+  std::vector<double> sx(cx.size()), sy(cy.size()), sz(cz.size());
+  for (size_t i = 0; i < cx.size(); ++i) sx[i] = std::sin(M_PI * cx[i]);
+  for (size_t i = 0; i < cy.size(); ++i) sy[i] = std::sin(M_PI * cy[i]);
+  for (size_t i = 0; i < cz.size(); ++i) sz[i] = std::sin(M_PI * cz[i]);
+  int64_t node = 0;
+  for (int64_t iz = 0; iz < NZ; ++iz)
+    for (int64_t iy = 0; iy < NY; ++iy)
+      for (int64_t ix = 0; ix < NX; ++ix, ++node) {
+        double x = cx[size_t(ix)], y = cy[size_t(iy)], z = cz[size_t(iz)];
+        if (deformation == Deformation::Sine) {
+          const double bump = 0.05 * sx[size_t(ix)] * sy[size_t(iy)] * sz[size_t(iz)];
+          x += bump;
+          y += bump;
+          z += bump;
+        }
+        mesh.coords[size_t(node)] = x;
+        mesh.coords[size_t(mesh.n_L + node)] = y;
+        mesh.coords[size_t(2 * mesh.n_L + node)] = z;
+        if (ix == 0 || ix == NX - 1 || iy == 0 || iy == NY - 1 || iz == 0 || iz == NZ - 1)
+          mesh.boundary_nodes.push_back(node);
+      }
+  return mesh;
+}
+
+// ------------------------------------------------------------ device
+Device::Device(int ordinal) { check(hxf_context_create(ordinal, nullptr, &ctx_)); }
+Device::~Device() {
+  if (ctx_) hxf_context_destroy(ctx_);
+}
+std::shared_ptr<Device> Device::get(int ordinal) {
+  static std::mutex mu;
+  static std::map<int, std::weak_ptr<Device>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto sp = cache[ordinal].lock();
+  if (!sp) {
+    sp = std::make_shared<Device>(ordinal);
+    cache[ordinal] = sp;
+  }
+  return sp;
+}
+
+DeviceBuffer::DeviceBuffer(std::shared_ptr<Device> dev, size_t count) : dev_(std::move(dev)), n_(count) {
+  void* p = nullptr;
+  check(hxf_malloc(dev_->ctx(), uint64_t(count) * 8, &p));
+  ptr_ = static_cast<double*>(p);
+}
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr_ && dev_) hxf_free(dev_->ctx(), ptr_);
+}
+void DeviceBuffer::upload(const double* src, size_t count) {
+  check(hxf_memcpy(dev_->ctx(), ptr_, src, uint64_t(count) * 8, 0));
+}
+void DeviceBuffer::download(double* dst, size_t count) const {
+  check(hxf_memcpy(dev_->ctx(), dst, ptr_, uint64_t(count) * 8, 1));
+}
+
+Operator::Operator(std::shared_ptr<Device> dev, const hxf_operator_desc& desc) : dev_(std::move(dev)) {
+  check(hxf_operator_create(dev_->ctx(), &desc, &op_));
+  size_ = hxf_operator_size(op_);
+}
+Operator::~Operator() {
+  if (op_) hxf_operator_destroy(op_);
+}
+void Operator::apply_host(const double* x, double* y) const {
+  check(hxf_operator_apply(op_, x, y, HXF_HOST, nullptr));
+}
+void Operator::apply_device(const double* x, double* y, void* stream) const {
+  check(hxf_operator_apply(op_, x, y, HXF_DEVICE, stream));
+}
+void Operator::diagonal_device(double* d) const { check(hxf_operator_diagonal(op_, d, HXF_DEVICE)); }
+
+SolveReport Operator::pcg(const double* b, const double* diag, const hxf_pcg_options& o, double* x,
+                          hxf_memspace space) const {
+  const int cap = (o.fixed_iterations >= 0 ? o.fixed_iterations : o.max_iter) + 2;
+  std::vector<double> hist(size_t(std::max(cap, 1)));
+  hxf_solve_report rep{};
+  rep.residual_history = hist.data();
+  rep.history_capacity = cap;
+  check(hxf_pcg(op_, b, diag, &o, x, space, &rep));
+  SolveReport out;
+  out.iterations = rep.iterations;
+  out.converged = rep.converged != 0;
+  out.residual_history.assign(hist.begin(), hist.begin() + std::min(cap, rep.iterations + 1));
+  out.apply_time_seconds = rep.apply_time_seconds;
+  out.total_time_seconds = rep.total_time_seconds;
+  return out;
+}
+
+// ------------------------------------------------------------ BP tables
+const char* bp_name(BpId bp) {
+  static const char* names[] = {"?", "bp1", "bp2", "bp3", "bp4", "bp5", "bp6"};
+  const int i = int(bp);
+  return (i >= 1 && i <= 6) ? names[i] : "?";
+}
+std::optional<BpId> parse_bp(const std::string& name) {
+  for (int i = 1; i <= 6; ++i)
+    if (name == bp_name(BpId(i))) return BpId(i);
+  return std::nullopt;
+}
+int bp_components(BpId bp) { return int(bp) % 2 == 1 ? 1 : 3; }
+int bp_quadrature_points(BpId bp, int p) { return int(bp) <= 4 ? p + 2 : p + 1; }
+QuadratureKind bp_quadrature_kind(BpId bp) {
+  return int(bp) <= 4 ? QuadratureKind::GaussLegendre : QuadratureKind::GaussLobattoLegendre;
+}
+double bp_alpha(BpId bp) { return int(bp) <= 2 ? 0.0 : 1.0; }
+double bp_beta(BpId bp) { return int(bp) <= 2 ? 1.0 : 0.0; }
+bool bp_has_constraints(BpId bp) { return int(bp) >= 3; }
+int64_t bp_dof_count(BpId bp, int p, std::array<int, 3> dims) {
+  int64_t count = 1;
+  for (int d = 0; d < 3; ++d) {
+    const int64_t axis = int64_t(dims[size_t(d)]) * p + 1;
+    count *= bp_has_constraints(bp) ? axis - 2 : axis;
+  }
+  return count * bp_components(bp);
+}
+double manufactured_solution(double x, double y, double z) {
+  return std::sin(M_PI * x) * std::sin(M_PI * y) * std::sin(M_PI * z);
+}
+double manufactured_rhs(double x, double y, double z) {
+  return 3.0 * M_PI * M_PI * manufactured_solution(x, y, z);
+}
+
+namespace {
+hxf_operator_desc base_desc(const HexMesh& mesh, const TensorBasis& basis, int m) {
+  hxf_operator_desc d{};
+  d.p = basis.p;
+  d.q = basis.q;
+  d.m = m;
+  d.num_elements = mesh.num_elements();
+  d.n_L = mesh.n_L;
+  d.interp1d = basis.interp1d.data();
+  d.grad1d = basis.grad1d.data();
+  d.qpoints = basis.quad.points.data();
+  d.indices = nullptr;  // structured box: G from the lattice (mesh.cpp:80-104)
+  d.dims[0] = mesh.dims[0];
+  d.dims[1] = mesh.dims[1];
+  d.dims[2] = mesh.dims[2];
+  d.qdata_space = HXF_DEVICE;
+  d.block = 8;
+  return d;
+}
+
+DeviceBuffer device_qdata(const std::shared_ptr<Device>& dev, const HexMesh& mesh,
+                          const TensorBasis& basis, const DeviceBuffer& d_coords,
+                          hxf_qdata_kind kind) {
+  const size_t n = size_t(mesh.num_elements()) * (kind == HXF_QDATA_MASS ? 1 : 6) * basis.num_qpts();
+  DeviceBuffer out(dev, n);
+  check(hxf_qdata_compute(dev->ctx(), basis.p, basis.q, basis.interp1d.data(), basis.grad1d.data(),
+                          basis.quad.weights.data(), mesh.num_elements(), mesh.n_L,
+                          d_coords.data(), nullptr, mesh.dims.data(), kind, out.data(),
+                          HXF_DEVICE));
+  return out;
+}
+}  // namespace
+
+const double* BpProblem::diagonal_device() {
+  if (!diag_ready) {
+    op->diagonal_device(d_diag.data());
+    diag_ready = true;
+  }
+  return d_diag.data();
+}
+
+// bp_setup (bench.cpp:64-119): mesh + basis on the host, geometric factors,
+// RHS mass apply and everything after on the GPU.
+std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
+  if (config.p < 1) throw std::invalid_argument("bp_setup: p must be >= 1");
+  for (int d : config.dims)
+    if (d < 1) throw std::invalid_argument("bp_setup: element counts must be >= 1");
+  auto prob = std::make_unique<BpProblem>();
+  prob->config = config;
+  prob->m = bp_components(config.bp);
+  prob->device = Device::get(config.device);
+  auto& dev = prob->device;
+  const int q = bp_quadrature_points(config.bp, config.p);
+  prob->mesh = build_mesh(config.dims[0], config.dims[1], config.dims[2], config.p,
+                          config.deformation);
+  prob->basis = make_basis(config.p, make_quadrature(bp_quadrature_kind(config.bp), q));
+  const HexMesh& mesh = prob->mesh;
+  const int64_t n_L = mesh.n_L;
+  const int m = prob->m;
+  const double alpha = bp_alpha(config.bp), beta = bp_beta(config.bp);
+
+  DeviceBuffer d_coords(dev, size_t(3 * n_L));
+  d_coords.upload(mesh.coords.data(), size_t(3 * n_L));
+  DeviceBuffer mass_qd = device_qdata(dev, mesh, prob->basis, d_coords, HXF_QDATA_MASS);
+  DeviceBuffer diff_qd;
+  if (alpha > 0) diff_qd = device_qdata(dev, mesh, prob->basis, d_coords, HXF_QDATA_DIFFUSION);
+  d_coords = DeviceBuffer();
+
+  if (bp_has_constraints(config.bp)) prob->constrained = mesh.boundary_nodes;
+
+  // manufactured fields at the nodes, b = B f with the unconstrained mass op
+  std::vector<double> f(size_t(m) * n_L);
+  prob->exact_nodal.assign(size_t(m) * n_L, 0.0);
+  const bool poisson = alpha > 0;
+  for (int64_t i = 0; i < n_L; ++i) {
+    const double x = mesh.coords[size_t(i)], y = mesh.coords[size_t(n_L + i)],
+                 z = mesh.coords[size_t(2 * n_L + i)];
+    const double u = manufactured_solution(x, y, z);
+    const double fv = poisson ? manufactured_rhs(x, y, z) : u;
+    for (int c = 0; c < m; ++c) {
+      f[size_t(c * n_L + i)] = fv;
+      prob->exact_nodal[size_t(c * n_L + i)] = u;
+    }
+  }
+  prob->rhs.assign(size_t(m) * n_L, 0.0);
+  {
+    hxf_operator_desc d = base_desc(mesh, prob->basis, m);
+    d.mass_qdata = mass_qd.data();
+    d.beta = 1.0;
+    Operator mass_op(dev, d);
+    mass_op.apply_host(f.data(), prob->rhs.data());
+  }
+  for (int c = 0; c < m; ++c)
+    for (int64_t i : prob->constrained) prob->rhs[size_t(c * n_L + i)] = 0.0;
+
+  hxf_operator_desc d = base_desc(mesh, prob->basis, m);
+  d.alpha = alpha;
+  d.beta = beta;
+  d.mass_qdata = beta > 0 ? mass_qd.data() : nullptr;
+  d.diff_qdata = alpha > 0 ? diff_qd.data() : nullptr;
+  d.constrained = prob->constrained.data();
+  d.n_constrained = int64_t(prob->constrained.size());
+  prob->op = std::make_unique<Operator>(dev, d);
+  prob->n_dofs = int64_t(m) * (n_L - int64_t(prob->constrained.size()));
+  prob->d_rhs = DeviceBuffer(dev, size_t(m) * n_L);
+  prob->d_rhs.upload(prob->rhs.data(), prob->rhs.size());
+  prob->d_diag = DeviceBuffer(dev, size_t(m) * n_L);
+  prob->d_x = DeviceBuffer(dev, size_t(m) * n_L);
+  return prob;
+}
+
+// solve_bp (bench.cpp:121-137), device resident.
+BpSolveResult solve_bp(BpProblem& problem, bool jacobi) {
+  hxf_pcg_options o{};
+  o.tol_rel = problem.config.tol_rel;
+  o.max_iter = problem.config.max_iter;
+  o.fixed_iterations = problem.config.fixed_iterations ? *problem.config.fixed_iterations : -1;
+  const double* diag = jacobi ? problem.diagonal_device() : nullptr;
+  BpSolveResult res;
+  res.report = problem.op->pcg(problem.d_rhs.data(), diag, o, problem.d_x.data(), HXF_DEVICE);
+  res.x.resize(size_t(problem.size()));
+  problem.d_x.download(res.x.data(), res.x.size());
+  return res;
+}
+
+// l2_error (bench.cpp:139-189): Gauss q=p+2 rule, element-wise interpolation.
+double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
+                const std::function<double(double, double, double)>& exact,
+                std::shared_ptr<Device> dev) {
+  const int p = mesh.p, n1 = p + 1, q = p + 2;
+  const TensorBasis eb = make_basis(p, make_quadrature(QuadratureKind::GaussLegendre, q));
+  const int64_t E = mesh.num_elements(), n_L = mesh.n_L;
+  const int S = n1 * n1 * n1, nq = q * q * q;
+  if (int64_t(u_h.size()) != int64_t(m) * n_L)
+    throw std::invalid_argument("l2_error: solution length mismatch");
+  // w det J at the Gauss points on the device
+  std::vector<double> wdet(size_t(E) * nq);
+  check(hxf_qdata_compute(dev->ctx(), p, q, eb.interp1d.data(), eb.grad1d.data(),
+                          eb.quad.weights.data(), E, n_L, mesh.coords.data(), nullptr,
+                          mesh.dims.data(), HXF_QDATA_MASS, wdet.data(), HXF_HOST));
+  // element values of coords (3) and solution (m) -> quadrature points
+  const int nfield = 3 + m;
+  std::vector<double> ev(size_t(nfield) * E * S);
+  const int64_t NX = mesh.nodes_per_axis[0], NY = mesh.nodes_per_axis[1];
+  for (int64_t e = 0; e < E; ++e) {
+    const int64_t ex = e % mesh.dims[0], ey = (e / mesh.dims[0]) % mesh.dims[1],
+                  ez = e / (int64_t(mesh.dims[0]) * mesh.dims[1]);
+    int s = 0;
+    for (int kz = 0; kz <= p; ++kz)
+      for (int ky = 0; ky <= p; ++ky)
+        for (int kx = 0; kx <= p; ++kx, ++s) {
+          const int64_t node = (ex * p + kx) + NX * ((ey * p + ky) + NY * (ez * p + kz));
+          for (int a = 0; a < 3; ++a)
+            ev[size_t((a * E + e) * S + s)] = mesh.coords[size_t(a * n_L + node)];
+          for (int c = 0; c < m; ++c)
+            ev[size_t(((3 + c) * E + e) * S + s)] = u_h[size_t(c * n_L + node)];
+        }
+  }
+  std::vector<double> qv(size_t(nfield) * E * nq);
+  check(hxf_basis_apply(dev->ctx(), p, q, eb.interp1d.data(), eb.grad1d.data(), HXF_INTERP,
+                        HXF_FORWARD, nfield * E, ev.data(), qv.data(), HXF_HOST));
+  double err2 = 0.0;
+  std::vector<double> diff2(static_cast<size_t>(nq));
+  for (int64_t e = 0; e < E; ++e) {
+    std::fill(diff2.begin(), diff2.end(), 0.0);
+    const double* xq = qv.data() + size_t(e) * nq;
+    const double* yq = qv.data() + size_t(E + e) * nq;
+    const double* zq = qv.data() + size_t(2 * E + e) * nq;
+    for (int c = 0; c < m; ++c) {
+      const double* uq = qv.data() + size_t((3 + c) * E + e) * nq;
+      for (int i = 0; i < nq; ++i) {
+        const double dlt = uq[i] - exact(xq[i], yq[i], zq[i]);
+        diff2[size_t(i)] += dlt * dlt;
+      }
+    }
+    for (int i = 0; i < nq; ++i) err2 += wdet[size_t(e * nq + i)] * diff2[size_t(i)];
+  }
+  return std::sqrt(err2);
+}
+
+// run_bench (bench.cpp:191-229): setup and diagonal untimed; the CG loop is
+// repeated 3 times in bench mode and the minimum (device) time recorded.
+BenchRecord run_bench(const BpConfig& config) {
+  if (config.threads < 1) throw std::invalid_argument("run_bench: threads must be >= 1");
+  auto prob = bp_setup(config);
+  const double* diag = prob->diagonal_device();
+  hxf_pcg_options o{};
+  o.tol_rel = config.tol_rel;
+  o.max_iter = config.max_iter;
+  o.fixed_iterations = config.fixed_iterations ? *config.fixed_iterations : -1;
+  const int reps = config.fixed_iterations ? 3 : 1;
+  double seconds = std::numeric_limits<double>::infinity(), apply_s = 0;
+  int iterations = 0;
+  for (int rep = 0; rep < reps; ++rep) {
+    const SolveReport r = prob->op->pcg(prob->d_rhs.data(), diag, o, prob->d_x.data(), HXF_DEVICE);
+    if (r.total_time_seconds < seconds) {
+      seconds = r.total_time_seconds;
+      apply_s = r.apply_time_seconds;
+    }
+    iterations = r.iterations;
+  }
+  BenchRecord rec;
+  rec.bp = bp_name(config.bp);
+  rec.p = config.p;
+  rec.q = prob->basis.q;
+  rec.E = prob->mesh.num_elements();
+  rec.n = prob->n_dofs;
+  rec.P = config.threads;
+  rec.iterations = iterations;
+  rec.seconds = seconds;
+  rec.dofs_rate = double(rec.n) * rec.iterations / rec.seconds;
+  rec.n_per_rank = double(rec.n) / rec.P;
+  rec.apply_seconds = apply_s;
+  return rec;
+}
+
+std::vector<double> assemble_dense(BpProblem& problem) {
+  const int64_t n = problem.size();
+  if (n > 20000)
+    throw std::invalid_argument("reference_assemble: problem too large (m*n_L = " +
+                                std::to_string(n) + " > 20000)");
+  std::vector<double> A(size_t(n) * n), e(size_t(n), 0.0), col(static_cast<size_t>(n));
+  DeviceBuffer de(problem.device, size_t(n)), dy(problem.device, size_t(n));
+  for (int64_t j = 0; j < n; ++j) {
+    e[size_t(j)] = 1.0;
+    de.upload(e.data(), e.size());
+    e[size_t(j)] = 0.0;
+    problem.op->apply_device(de.data(), dy.data());
+    dy.download(col.data(), col.size());
+    for (int64_t i = 0; i < n; ++i) A[size_t(i * n + j)] = col[size_t(i)];
+  }
+  return A;
+}
+
+}  // namespace hexfem_b200

@@ -1,0 +1,201 @@
+// Host-side C++ mirror of the reference's (hexfem) BP API, B200-native
+// underneath: setup tables are built on the host exactly as the reference
+// builds them (so meshes, indices and RHS agree bit for bit), every
+// operator-sized computation runs on the GPU through the hxf C-ABI
+// (include/hxf.h).  Names follow the reference's public API
+// (proj/include/hexfem/*.hpp) so callers switch by namespace.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hxf.h"
+
+namespace hexfem_b200 {
+
+// ---- errors: hxf status -> the reference's exception types ----------------
+void check(int status);
+
+// ---- quadrature / basis (quadrature.hpp:7-22, tensor_basis.hpp:17-33) ----
+enum class QuadratureKind { GaussLegendre, GaussLobattoLegendre };
+struct QuadratureRule {
+  QuadratureKind kind = QuadratureKind::GaussLegendre;
+  int q = 0;
+  std::vector<double> points, weights;
+};
+QuadratureRule make_quadrature(QuadratureKind kind, int q);
+
+struct TensorBasis {
+  int p = 0, q = 0;
+  std::vector<double> nodes;
+  QuadratureRule quad;
+  std::vector<double> interp1d, grad1d;  // q x (p+1) row-major
+  bool collocated = false;
+  int num_nodes() const { return (p + 1) * (p + 1) * (p + 1); }
+  int num_qpts() const { return q * q * q; }
+};
+TensorBasis make_basis(int p, const QuadratureRule& quad);
+
+// ---- mesh (mesh.hpp:9-41) ------------------------------------------------
+enum class Deformation { None, Sine };
+struct HexMesh {
+  std::array<int, 3> dims{};
+  int p = 1;
+  std::array<int64_t, 3> nodes_per_axis{};
+  int64_t n_L = 0;
+  std::vector<double> coords;  // 3*n_L component-major
+  std::vector<int64_t> boundary_nodes;
+  Deformation deformation = Deformation::None;
+  int64_t num_elements() const { return int64_t(dims[0]) * dims[1] * dims[2]; }
+  int nodes_per_elem() const { return (p + 1) * (p + 1) * (p + 1); }
+};
+HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation = Deformation::None);
+
+// ---- device context -------------------------------------------------------
+class Device {
+ public:
+  explicit Device(int ordinal = 0);
+  ~Device();
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  hxf_ctx* ctx() const { return ctx_; }
+  static std::shared_ptr<Device> get(int ordinal = 0);  // process-wide per ordinal
+
+ private:
+  hxf_ctx* ctx_ = nullptr;
+};
+
+// Device buffer owned by a Device context.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(std::shared_ptr<Device> dev, size_t count);
+  ~DeviceBuffer();
+  DeviceBuffer(DeviceBuffer&& o) noexcept { swap(o); }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    swap(o);
+    return *this;
+  }
+  double* data() const { return ptr_; }
+  size_t size() const { return n_; }
+  void upload(const double* src, size_t count);
+  void download(double* dst, size_t count) const;
+
+ private:
+  void swap(DeviceBuffer& o) {
+    std::swap(dev_, o.dev_);
+    std::swap(ptr_, o.ptr_);
+    std::swap(n_, o.n_);
+  }
+  std::shared_ptr<Device> dev_;
+  double* ptr_ = nullptr;
+  size_t n_ = 0;
+};
+
+// ---- BP problems (bench.hpp:16-58) --------------------------------------
+enum class BpId { BP1 = 1, BP2, BP3, BP4, BP5, BP6 };
+const char* bp_name(BpId bp);
+std::optional<BpId> parse_bp(const std::string& name);
+int bp_components(BpId bp);
+int bp_quadrature_points(BpId bp, int p);
+QuadratureKind bp_quadrature_kind(BpId bp);
+double bp_alpha(BpId bp);
+double bp_beta(BpId bp);
+bool bp_has_constraints(BpId bp);
+int64_t bp_dof_count(BpId bp, int p, std::array<int, 3> dims);
+double manufactured_solution(double x, double y, double z);
+double manufactured_rhs(double x, double y, double z);
+
+struct BpConfig {
+  BpId bp = BpId::BP1;
+  int p = 1;
+  std::array<int, 3> dims{1, 1, 1};
+  Deformation deformation = Deformation::None;
+  int threads = 1;  // accepted for API compatibility; the GPU is the worker
+  std::optional<int> fixed_iterations = 20;
+  double tol_rel = 1e-8;
+  int max_iter = 2000;
+  int device = 0;
+};
+
+struct SolveReport {
+  int iterations = 0;
+  std::vector<double> residual_history;
+  bool converged = false;
+  double apply_time_seconds = 0.0;  // device time in the operator kernel
+  double total_time_seconds = 0.0;  // device time of the whole solve
+};
+
+// The operator handle (MatFreeOperator analogue) owns its device data.
+class Operator {
+ public:
+  Operator(std::shared_ptr<Device> dev, const hxf_operator_desc& desc);
+  ~Operator();
+  Operator(const Operator&) = delete;
+  Operator& operator=(const Operator&) = delete;
+  hxf_op* handle() const { return op_; }
+  int64_t size() const { return size_; }
+  void apply_host(const double* x, double* y) const;
+  void apply_device(const double* x, double* y, void* stream = nullptr) const;
+  void diagonal_device(double* d) const;
+  SolveReport pcg(const double* b, const double* diag, const hxf_pcg_options& o, double* x,
+                  hxf_memspace space) const;
+
+ private:
+  std::shared_ptr<Device> dev_;
+  hxf_op* op_ = nullptr;
+  int64_t size_ = 0;
+};
+
+struct BpProblem {
+  BpConfig config;
+  HexMesh mesh;
+  TensorBasis basis;
+  int m = 1;
+  int64_t n_dofs = 0;
+  std::vector<int64_t> constrained;
+  std::vector<double> rhs;          // B f, constrained entries zeroed
+  std::vector<double> exact_nodal;  // nodal interpolant of u*
+  std::shared_ptr<Device> device;
+  std::unique_ptr<Operator> op;
+  DeviceBuffer d_rhs, d_diag, d_x, d_b;
+  bool diag_ready = false;
+  int64_t size() const { return int64_t(m) * mesh.n_L; }
+  const double* diagonal_device();  // computed once, cached
+};
+
+std::unique_ptr<BpProblem> bp_setup(const BpConfig& config);
+
+struct BpSolveResult {
+  std::vector<double> x;
+  SolveReport report;
+};
+BpSolveResult solve_bp(BpProblem& problem, bool jacobi = true);
+
+double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
+                const std::function<double(double, double, double)>& exact,
+                std::shared_ptr<Device> dev);
+
+struct BenchRecord {
+  std::string bp;
+  int p = 0, q = 0;
+  int64_t E = 0, n = 0;
+  int P = 1;
+  int iterations = 0;
+  double seconds = 0, dofs_rate = 0, n_per_rank = 0;
+  double apply_seconds = 0;  // device time in the operator kernel, same rep
+};
+BenchRecord run_bench(const BpConfig& config);
+
+// Dense matrix of the operator by applying it to unit vectors on the device
+// (the reference's reference_assemble is a dense quadrature loop, oracle only;
+// operator.cpp:258-349).  Rejected above 20000 unknowns like the reference.
+std::vector<double> assemble_dense(BpProblem& problem);
+
+}  // namespace hexfem_b200

@@ -40,6 +40,14 @@ CASES = [
 ]
 
 
+ANCHORS = [
+    ("bp1", 3, (16, 16, 16), "none", False), ("bp1", 3, (16, 16, 16), "sine", False),
+    ("bp5", 7, (8, 8, 8), "sine", True), ("bp3", 7, (8, 8, 8), "sine", True),
+    ("bp6", 5, (4, 4, 4), "sine", True), ("bp5", 7, (8, 8, 8), "none", True),
+    ("bp2", 3, (4, 4, 4), "sine", True), ("bp4", 4, (3, 3, 3), "sine", True),
+]
+
+
 def main() -> None:
     if not oracle.available("reference"):
         raise SystemExit("oracle/_ref not built: run `make -C oracle ref` first")
@@ -94,6 +102,22 @@ def main() -> None:
                     p, kind, q, mode, direction, ne, u, impl="reference")
     np.savez_compressed(OUT / "tables.npz", **tabs)
     print("tables.npz")
+
+    # CG iteration-count anchors (tol 1e-8) at sizes too large to store
+    # vectors for: the +-1 iteration targets of the GPU solver.
+    import json
+    anchors = []
+    for bp, p, dims, deform, jacobi in ANCHORS:
+        pr = oracle.setup(bp, p, dims, deform, threads=8, impl="reference")
+        _, rep = pr.solve(tol=1e-8, jacobi=jacobi)
+        anchors.append({"bp": bp, "p": p, "dims": list(dims), "deform": deform,
+                        "jacobi": jacobi, "tol": 1e-8, "iterations": rep["iterations"],
+                        "converged": rep["converged"],
+                        "final_residual": float(rep["residual_history"][-1]),
+                        "norm_b": float(rep["residual_history"][0]), "n": pr.n})
+        print(anchors[-1])
+    with open(OUT / "anchors.json", "w") as f:
+        json.dump(anchors, f, indent=1)
 
 
 if __name__ == "__main__":
