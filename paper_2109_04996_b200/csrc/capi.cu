@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -119,6 +120,14 @@ int num_sms() {
 }
 
 void count_launch(int n) { g_launches += n; }
+
+bool pencil_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("HXF_OP_KERNEL");
+    return v && std::string(v) == "generic";
+  }();
+  return off;
+}
 
 int max_op_grid() { return num_sms() * 32; }
 

@@ -57,6 +57,8 @@ HXF_DECL_P(16)
 #undef HXF_DECL_P
 
 int num_sms();
+// HXF_OP_KERNEL=generic forces the generic fused kernel (A/B comparisons).
+bool pencil_disabled();
 void count_launch(int n = 1);
 
 }  // namespace hxf

@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "op_kernel.cuh"
+#include "op_pencil.cuh"
 
 namespace hxf {
 namespace {
@@ -43,9 +44,47 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
   return cudaGetLastError();
 }
 
+// Collocated diffusion fast path (op_pencil.cuh) when its single-stage
+// footprint leaves room for at least two CTAs per SM.
+template <class T>
+cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_pencil_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  PencilMats<T::P> mats;
+  std::memcpy(mats.D, D, sizeof(double) * T::P * T::P);
+  const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
+  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int P, int NC>
+constexpr bool use_pencil() {
+  return P <= 10 && PencilTraits<P, NC>::SMEM_BYTES <= 112 * 1024;
+}
+
 template <int P, int Q, bool INTERP>
 cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const double* D,
                   cudaStream_t s, int* g) {
+  if constexpr (!INTERP) {
+    if (qk == 1 && NC == 1 && use_pencil<P, 1>() && !pencil_disabled())
+      return run_pencil<PencilTraits<P, 1>>(prm, D, s, g);
+    if (qk == 1 && NC == 3 && use_pencil<P, 3>() && !pencil_disabled())
+      return run_pencil<PencilTraits<P, 3>>(prm, D, s, g);
+  }
   if (NC == 1 && qk == 1) return run<typename Pick<P, Q, 1, INTERP, 1>::T>(prm, B, D, s, g);
   if (NC == 1 && qk == 2) return run<typename Pick<P, Q, 1, INTERP, 2>::T>(prm, B, D, s, g);
   if (NC == 3 && qk == 1) return run<typename Pick<P, Q, 3, INTERP, 1>::T>(prm, B, D, s, g);
