@@ -121,6 +121,14 @@ int num_sms() {
 
 void count_launch(int n) { g_launches += n; }
 
+int ablate_bits() {
+  static const int bits = [] {
+    const char* v = std::getenv("HXF_ABLATE");
+    return v ? std::atoi(v) : 0;
+  }();
+  return bits;
+}
+
 bool pencil_disabled() {
   static const bool off = [] {
     const char* v = std::getenv("HXF_OP_KERNEL");
@@ -236,6 +244,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.cons_mode = op->cons_mode;
   prm.cons_mask = op->d_mask;
   prm.stop = stop;
+  prm.ablate = ablate_bits();
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
     const double coef = pass == 0 ? op->alpha : op->beta;

@@ -24,6 +24,7 @@ struct OpParams {
   double* dot_partials;      // per-CTA partial of x_masked . y, or nullptr
   const int* stop;           // device flag: skip the whole kernel when set (PCG)
   double coef;               // alpha (diffusion) or beta (mass)
+  int ablate;                // measurement-only ablation bits (HXF_ABLATE), 0 in production
 };
 
 // Launch the fused operator kernel instance for (P, Q, NC, interp, qk);
@@ -59,6 +60,7 @@ HXF_DECL_P(16)
 int num_sms();
 // HXF_OP_KERNEL=generic forces the generic fused kernel (A/B comparisons).
 bool pencil_disabled();
+int ablate_bits();
 void count_launch(int n = 1);
 
 }  // namespace hxf

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(T::NT)
     mbar_init(&qbar, 1);
     fence_mbar_init();
     policy = l2_evict_first_policy();
-    if ((int64_t)blockIdx.x < nsteps) issue_qdata(blockIdx.x);
+    if ((int64_t)blockIdx.x < nsteps && !(prm.ablate & 4)) issue_qdata(blockIdx.x);
   }
   __syncthreads();
 
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(T::NT)
         u[k] = 0.0;
         if (active) {
           const int64_t node = node_at(k);
-          u[k] = is_cons(node, k) ? 0.0 : __ldg(xc + node);
+          u[k] = (prm.ablate & 1) ? 1.0 : (is_cons(node, k) ? 0.0 : __ldg(xc + node));
         }
         if (active_slot) SA[k * PL + lb * RS + la] = u[k];
       }
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(T::NT)
           *reinterpret_cast<double2*>(rp + a) = make_double2(g[a], g[a + 1]);
         if (P & 1) rp[P - 1] = g[P - 1];
       }
-      if (c == 0) mbar_wait(&qbar, (uint32_t)(it & 1));
+      if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
       __syncthreads();
 
       // ---- pointwise: z-derivative from registers + QFunction (qfunction.cpp:135-162) ----
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(T::NT)
       if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
       __syncthreads();
       // factors consumed: stream the next step's in while we transpose
-      if (c == NC - 1 && tid == 0 && step + G < nsteps) issue_qdata(step + G);
+      if (c == NC - 1 && tid == 0 && step + G < nsteps && !(prm.ablate & 4)) issue_qdata(step + G);
 
       // ---- transposed y-pencil (in place, slab B) and x-pencil (in place, slab A) ----
       if (active_slot) {
@@ -254,7 +254,9 @@ __global__ void __launch_bounds__(T::NT)
           const int sp = k * PL + lb * RS + la;
           const double yk = prm.coef * (SA[sp] + SB[sp] + s);
           const int64_t node = node_at(k);
-          if (is_cons(node, k)) {
+          if (prm.ablate & 2) {
+            dot_acc += u[k] * yk;
+          } else if (is_cons(node, k)) {
             yc[node] = __ldg(xc + node);
           } else {
             red_add(yc + node, yk);
