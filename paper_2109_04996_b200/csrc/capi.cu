@@ -245,6 +245,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.cons_mask = op->d_mask;
   prm.stop = stop;
   prm.ablate = ablate_bits();
+  prm.D = op->d_G;
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
     const double coef = pass == 0 ? op->alpha : op->beta;

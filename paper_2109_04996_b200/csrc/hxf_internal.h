@@ -25,6 +25,7 @@ struct OpParams {
   const int* stop;           // device flag: skip the whole kernel when set (PCG)
   double coef;               // alpha (diffusion) or beta (mass)
   int ablate;                // measurement-only ablation bits (HXF_ABLATE), 0 in production
+  const double* D;           // device copy of the 1-D derivative matrix (collocated path)
 };
 
 // Launch the fused operator kernel instance for (P, Q, NC, interp, qk);

@@ -60,20 +60,27 @@ cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int
     if (nb < 1) return cudaErrorInvalidConfiguration;
     max_ctas = nb * num_sms();
   }
-  PencilMats<T::P> mats;
-  std::memcpy(mats.D, D, sizeof(double) * T::P * T::P);
+  static_assert(T::GM == 0 || T::GM == 1, "gather mode");
+  (void)D;
+  if (!prm.D) return cudaErrorInvalidValue;
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
   const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
+  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int P, int NC>
 constexpr bool use_pencil() {
-  return P <= 10 && PencilTraits<P, NC>::SMEM_BYTES <= 112 * 1024;
+  return P <= 10 && PencilTraits<P, NC, 0>::SMEM_BYTES <= 112 * 1024;
+}
+
+template <int P, int NC>
+cudaError_t run_pencil_gm(const OpParams& prm, const double* D, cudaStream_t s, int* g) {
+  if (!prm.idx && prm.cons_mode != 2) return run_pencil<PencilTraits<P, NC, 0>>(prm, D, s, g);
+  return run_pencil<PencilTraits<P, NC, 1>>(prm, D, s, g);
 }
 
 template <int P, int Q, bool INTERP>
@@ -81,9 +88,9 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
                   cudaStream_t s, int* g) {
   if constexpr (!INTERP) {
     if (qk == 1 && NC == 1 && use_pencil<P, 1>() && !pencil_disabled())
-      return run_pencil<PencilTraits<P, 1>>(prm, D, s, g);
+      return run_pencil_gm<P, 1>(prm, D, s, g);
     if (qk == 1 && NC == 3 && use_pencil<P, 3>() && !pencil_disabled())
-      return run_pencil<PencilTraits<P, 3>>(prm, D, s, g);
+      return run_pencil_gm<P, 3>(prm, D, s, g);
   }
   if (NC == 1 && qk == 1) return run<typename Pick<P, Q, 1, INTERP, 1>::T>(prm, B, D, s, g);
   if (NC == 1 && qk == 2) return run<typename Pick<P, Q, 1, INTERP, 2>::T>(prm, B, D, s, g);

@@ -2,20 +2,24 @@
 //   y = G^T D^T S D G x   on GLL-collocated elements (interp1d == I).
 //
 // Same contract as op_apply_kernel (op_kernel.cuh) — masked gather, RED
-// scatter, constrained y = x, fused p.Ap partials — restructured for issue
-// efficiency on sm_100a:
-//   * every 1-D contraction is a register-resident "pencil": one thread owns a
-//     whole x-, y- or z-line of the element and multiplies it by the 1-D
-//     derivative matrix held in the kernel-parameter constant bank (DFMA with
-//     constant operands, no shared-memory matrix loads);
-//   * lines move between threads through two padded shared slabs, updated in
-//     place (rows padded to 2 mod 4 doubles, planes skewed by half a bank
-//     cycle, so the x-line LDS.128 and the y-line LDS.64 are conflict-free);
-//   * the element's geometric factors (6 P^3 doubles) arrive by one bulk
-//     async copy (TMA engine, L2 evict_first) issued as soon as the previous
-//     element has consumed its factors, i.e. a full transpose phase plus the
-//     next gather ahead of use, in a single stage — half the shared memory of
-//     a double buffer, so more CTAs (and more bytes in flight) per SM.
+// scatter, constrained y = x, fused p.Ap partials — restructured for the
+// sm_100a memory system.  Per work item (element, component) four phases,
+// one __syncthreads each, every 1-D contraction a register "pencil":
+//   F  thread (a,b) reads the x-line (j=a,k=b) and the y-line (i=a,k=b) of
+//      the gathered slab A and applies D to both, one D row (broadcast from
+//      shared memory) feeding two pencils: g0 -> slab C, g1 -> slab B;
+//   P  thread (i,j) re-reads its z-line of A, writes the NEXT item's masked
+//      z-line into A (software-pipelined gather: its global loads were issued
+//      one item earlier), applies D along z in registers and the pointwise
+//      QFunction with the geometric factors from shared memory; v0 -> C,
+//      v1 -> B in place; p.(A p) accumulates as grad u . S grad u;
+//   T  thread (a,b) applies D^T to its x-line of C and y-line of B, in place;
+//   Z  thread (i,j) applies D^T along z, sums, and scatters with FP64 RED.
+// Slab rows are XOR-rotated in 16-byte chunks for p = 7 (padded otherwise)
+// and planes skewed by half a bank cycle, so every shared access is
+// conflict-free.  The element's geometric factors (6 P^3 doubles) arrive by
+// one bulk async copy (TMA engine, L2 evict_first) issued as soon as phase P
+// of the previous element has consumed its factors.
 // Reference semantics: proj/src/operator.cpp:64-144 (see op_kernel.cuh).
 #pragma once
 #include "hxf_device.cuh"
@@ -30,31 +34,62 @@ __host__ __device__ constexpr int pencil_row_stride(int P) {
   return ((P + 1) / 4) * 4 + 2 >= P ? ((P + 1) / 4) * 4 + 2 : ((P + 1) / 4) * 4 + 6;
 }
 
-template <int P_, int NC_>
+template <int P_, int NC_, int GM_>
 struct PencilTraits {
-  static constexpr int P = P_, NC = NC_, PP = P * P, P3 = P * P * P;
+  // GM 0: structured box, constraints none/box boundary (lattice-computed G);
+  // GM 1: general — int32 index table and/or constraint bitmask.
+  static constexpr int P = P_, NC = NC_, GM = GM_, PP = P * P, P3 = P * P * P;
   static constexpr int EPB = PP >= 64 ? 1 : (PP == 25 ? 5 : (PP == 36 ? 3 : (PP == 49 ? 2 : 64 / PP)));
   static constexpr int NT = pencil_round_up(EPB * PP, 32);
-  static constexpr int RS = pencil_row_stride(P);
+  static constexpr bool SWZ = (P == 8);  // XOR-rotated 64-byte rows
+  static constexpr int RS = SWZ ? 8 : pencil_row_stride(P);
   static constexpr int PL = P * RS + 8;  // plane stride: +64 B skews consecutive planes by 16 banks
   static constexpr int SLAB = P * PL;    // doubles per element slab
   static constexpr int QDS = 6 * P3;     // geometric factors per element (even)
-  static constexpr int OFF_QD = 0;
+  static constexpr int DR = pencil_round_up(P, 2);  // matrix row stride (16-byte rows)
+  static constexpr int OFF_D = 0;                   // [P][DR] D, then [P][DR] D^T
+  static constexpr int OFF_QD = 2 * P * DR;
   static constexpr int OFF_A = OFF_QD + EPB * QDS;
   static constexpr int OFF_B = OFF_A + EPB * SLAB;
-  static constexpr int SMEM_BYTES = (OFF_B + EPB * SLAB) * 8;
+  static constexpr int OFF_C = OFF_B + EPB * SLAB;
+  static constexpr int SMEM_BYTES = (OFF_C + EPB * SLAB) * 8;
+
+  // slab offset of point (i, j, k) — x index i, y index j, plane k
+  __device__ static __forceinline__ int off(int k, int j, int i) {
+    if constexpr (SWZ) return k * PL + j * RS + 2 * (((i >> 1) + (j >> 1)) & 3) + (i & 1);
+    return k * PL + j * RS + i;
+  }
+  // slab offset of the 16-byte chunk holding x indices (2c, 2c+1) of row (j, k)
+  __device__ static __forceinline__ int chunk(int k, int j, int c) {
+    if constexpr (SWZ) return k * PL + j * RS + 2 * ((c + (j >> 1)) & 3);
+    return k * PL + j * RS + 2 * c;
+  }
+};
+
+// Lattice placement of one (element, lane) work item: the z-line's first
+// node (or the element id in table mode) and which of its P nodes are
+// constrained (bit k).
+struct PencilGeo {
+  int64_t key;     // node of (i, j, k = 0) (structured box) or element id (table)
+  uint32_t cmask;  // bit k: node k of the z-line is constrained
+  bool active;
 };
 
 template <int P>
-struct PencilMats {
-  double D[P * P];  // grad1d (q = p+1 GLL), row = quadrature point
-};
+__device__ __forceinline__ void load_row(const double* src, double* dst) {
+#pragma unroll
+  for (int a = 0; a + 1 < P; a += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(src + a);
+    dst[a] = v.x;
+    dst[a + 1] = v.y;
+  }
+  if (P & 1) dst[P - 1] = src[P - 1];
+}
 
 template <class T>
-__global__ void __launch_bounds__(T::NT)
-    op_pencil_kernel(const OpParams prm, const PencilMats<T::P> mats) {
+__global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   constexpr int P = T::P, PP = T::PP, P3 = T::P3, EPB = T::EPB, NT = T::NT, NC = T::NC;
-  constexpr int RS = T::RS, PL = T::PL;
+  constexpr int DR = T::DR;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_scratch[NT / 32 + 1];
@@ -65,13 +100,23 @@ __global__ void __launch_bounds__(T::NT)
   const int l = tid - slot * PP;
   const bool active_slot = slot < EPB;
   const int la = l % P, lb = l / P;  // (i,j) | (j,k) | (i,k) depending on the phase
+  const double* sD = smem + T::OFF_D;
+  const double* sDT = smem + T::OFF_D + P * DR;
   double* sQD = smem + T::OFF_QD;
   double* SA = smem + T::OFF_A + (active_slot ? slot : 0) * T::SLAB;
   double* SB = smem + T::OFF_B + (active_slot ? slot : 0) * T::SLAB;
+  double* SC = smem + T::OFF_C + (active_slot ? slot : 0) * T::SLAB;
   const double* qd_el = sQD + (active_slot ? slot : 0) * T::QDS;
+
+  for (int t = tid; t < P * P; t += NT) {
+    const int r = t / P, c = t % P;
+    smem[T::OFF_D + r * DR + c] = prm.D[t];           // D[r][c]
+    smem[T::OFF_D + P * DR + c * DR + r] = prm.D[t];  // D^T[c][r]
+  }
 
   const int64_t nsteps = (prm.E + EPB - 1) / EPB;
   const int64_t G = gridDim.x;
+  const int64_t NXY = prm.NX * prm.NY;
   uint64_t policy = 0;
   auto issue_qdata = [&](int64_t s) {
     const int64_t e0 = s * EPB;
@@ -86,110 +131,125 @@ __global__ void __launch_bounds__(T::NT)
     policy = l2_evict_first_policy();
     if ((int64_t)blockIdx.x < nsteps && !(prm.ablate & 4)) issue_qdata(blockIdx.x);
   }
-  __syncthreads();
 
-  const int64_t NXY = prm.NX * prm.NY;
-  double dot_acc = 0.0;
-  int it = 0;
-  for (int64_t step = blockIdx.x; step < nsteps; step += G, ++it) {
+  auto node_of = [&](const PencilGeo& g, int k) -> int64_t {
+    if constexpr (T::GM == 0) return g.key + k * NXY;
+    return prm.idx ? (int64_t)prm.idx[g.key * P3 + la + P * (lb + P * k)] : g.key + k * NXY;
+  };
+  auto geometry = [&](int64_t step) {
+    PencilGeo g{};
     const int64_t e = step * EPB + slot;
-    const bool active = active_slot && e < prm.E;
-    // node of (i = la, j = lb, k = 0) and whether the element touches the
-    // constrained set (structured box boundary, or any bitmask mode)
-    int64_t base = 0, ix0 = 0, iy0 = 0, iz0 = 0;
-    bool edge = prm.cons_mode != 0;
-    if (active && !prm.idx) {
+    g.active = active_slot && step < nsteps && e < prm.E;
+    if (!g.active) return g;
+    if (T::GM == 1 && prm.idx) {
+      g.key = e;
+    } else {
       const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      ix0 = ex * (P - 1) + la;
-      iy0 = ey * (P - 1) + lb;
-      iz0 = ez * (P - 1);
-      base = ix0 + prm.NX * iy0 + NXY * iz0;
-      if (prm.cons_mode == 1)
-        edge = ex == 0 || ey == 0 || ez == 0 || ex == prm.nx - 1 || ey == prm.ny - 1 ||
-               (ez + 1) * (P - 1) == prm.NZ - 1;
+      const int64_t ix = ex * (P - 1) + la, iy = ey * (P - 1) + lb, iz = ez * (P - 1);
+      g.key = ix + prm.NX * iy + NXY * iz;
+      if (T::GM == 0 && prm.cons_mode == 1) {
+        if (ix == 0 || ix == prm.NX - 1 || iy == 0 || iy == prm.NY - 1) g.cmask = (1u << P) - 1;
+        if (iz == 0) g.cmask |= 1u;
+        if (iz + P - 1 == prm.NZ - 1) g.cmask |= 1u << (P - 1);
+      }
     }
-    auto node_at = [&](int k) -> int64_t {
-      return prm.idx ? (int64_t)prm.idx[e * P3 + la + P * (lb + P * k)] : base + k * NXY;
-    };
-    auto is_cons = [&](int64_t node, int k) -> bool {
-      if (!edge) return false;
-      if (prm.cons_mode == 2) return (prm.cons_mask[node >> 5] >> (node & 31)) & 1u;
-      return ix0 == 0 || ix0 == prm.NX - 1 || iy0 == 0 || iy0 == prm.NY - 1 || iz0 + k == 0 ||
-             iz0 + k == prm.NZ - 1;
-    };
-
-#pragma unroll 1
-    for (int c = 0; c < NC; ++c) {
-      const double* xc = prm.x + c * prm.n_L;
-      double* yc = prm.y + c * prm.n_L;
-      if (c > 0 || it > 0) __syncthreads();  // slabs free (previous final phase done)
-
-      // ---- gather z-line (i,j) = (la,lb); masked copy into slab A ----
-      double u[P];
+    if (T::GM == 1 && prm.cons_mode == 2) {
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        u[k] = 0.0;
-        if (active) {
-          const int64_t node = node_at(k);
-          u[k] = (prm.ablate & 1) ? 1.0 : (is_cons(node, k) ? 0.0 : __ldg(xc + node));
-        }
-        if (active_slot) SA[k * PL + lb * RS + la] = u[k];
+        const int64_t node = node_of(g, k);
+        g.cmask |= ((prm.cons_mask[node >> 5] >> (node & 31)) & 1u) << k;
       }
-      __syncthreads();
+    }
+    return g;
+  };
+  // Work item q (0, 1, 2, ... for this CTA) = (element step, component).
+  auto item_step = [&](int q) -> int64_t { return (int64_t)blockIdx.x + (int64_t)(q / NC) * G; };
+  // raw (unmasked) z-line loads of work item (g, component c) into xn[]
+  auto load_line = [&](const PencilGeo& g, int c, double* xn) {
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      xn[k] = (g.active && !(prm.ablate & 1)) ? __ldg(prm.x + c * prm.n_L + node_of(g, k)) : 1.0;
+  };
+  auto store_line = [&](const PencilGeo& g, const double* xn) {
+    if (!active_slot) return;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      SA[T::off(k, lb, la)] = (g.active && !((g.cmask >> k) & 1u)) ? xn[k] : 0.0;
+  };
 
-      // ---- y-pencil (i,k) = (la,lb): g1 = D along y, into slab B ----
+  // prologue: item 0 into slab A, item 1's loads in flight
+  PencilGeo gcur = geometry(blockIdx.x);
+  double xn[P];
+  load_line(gcur, 0, xn);
+  store_line(gcur, xn);
+  PencilGeo gpf = NC > 1 ? gcur : geometry(item_step(1));  // geometry of the prefetched item
+  load_line(gpf, 1 % NC, xn);
+  __syncthreads();  // mbarrier init, matrices and slab A visible
+
+  double dot_acc = 0.0;
+  int it = 0, q = 0;
+#pragma unroll 1
+  for (int64_t step = blockIdx.x; step < nsteps; step += G, ++it) {
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c, ++q) {
+      double* yc = prm.y + c * prm.n_L;
+      const double* xc = prm.x + c * prm.n_L;
+
+      // ---- F: D along x (-> C) and y (-> B) from slab A, one D row per two pencils ----
       if (active_slot) {
-        double col[P];
-#pragma unroll
-        for (int b = 0; b < P; ++b) col[b] = SA[lb * PL + b * RS + la];
-#pragma unroll
-        for (int o = 0; o < P; ++o) {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < P; ++b) s += mats.D[o * P + b] * col[b];
-          SB[lb * PL + o * RS + la] = s;
-        }
-      }
-      __syncthreads();
-      // ---- x-pencil (j,k) = (la,lb): g0 = D along x, in place in slab A ----
-      if (active_slot) {
-        double row[P];
-        double* rp = SA + lb * PL + la * RS;
+        double row[P], col[P];
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(rp + a);
+          const double2 v = *reinterpret_cast<const double2*>(SA + T::chunk(lb, la, a / 2));
           row[a] = v.x;
           row[a + 1] = v.y;
         }
-        if (P & 1) row[P - 1] = rp[P - 1];
-        double g[P];
+        if (P & 1) row[P - 1] = SA[T::off(lb, la, P - 1)];
+#pragma unroll
+        for (int b = 0; b < P; ++b) col[b] = SA[T::off(lb, b, la)];
+        double gx[P];
 #pragma unroll
         for (int o = 0; o < P; ++o) {
-          double s = 0.0;
+          double d[P];
+          load_row<P>(sD + o * DR, d);
+          double sx = 0.0, sy = 0.0;
 #pragma unroll
-          for (int a = 0; a < P; ++a) s += mats.D[o * P + a] * row[a];
-          g[o] = s;
+          for (int a = 0; a < P; ++a) {
+            sx += d[a] * row[a];
+            sy += d[a] * col[a];
+          }
+          gx[o] = sx;
+          SB[T::off(lb, o, la)] = sy;
         }
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2)
-          *reinterpret_cast<double2*>(rp + a) = make_double2(g[a], g[a + 1]);
-        if (P & 1) rp[P - 1] = g[P - 1];
+          *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(gx[a], gx[a + 1]);
+        if (P & 1) SC[T::off(lb, la, P - 1)] = gx[P - 1];
       }
       if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
       __syncthreads();
 
-      // ---- pointwise: z-derivative from registers + QFunction (qfunction.cpp:135-162) ----
+      // ---- P: z-line of A, next item's gather into A, D along z + QFunction ----
+      double u[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) u[k] = SA[T::off(k, lb, la)];
+      store_line(gpf, xn);  // item q+1's masked z-line (this thread's column only)
+      gpf = ((q + 2) / NC == (q + 1) / NC && NC > 1) ? gpf : geometry(item_step(q + 2));
+      load_line(gpf, (q + 2) % NC, xn);  // item q+2 lands while items q, q+1 compute
       double v2[P];
+      double energy = 0.0;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
+        double d[P];
+        load_row<P>(sD + k * DR, d);
         double g2 = 0.0;
 #pragma unroll
-        for (int cc = 0; cc < P; ++cc) g2 += mats.D[k * P + cc] * u[cc];
-        const int sp = k * PL + lb * RS + la;
+        for (int cc = 0; cc < P; ++cc) g2 += d[cc] * u[cc];
+        const int sp = T::off(k, lb, la);
         const int pt = k * PP + lb * P + la;
-        const double g0 = SA[sp], g1 = SB[sp];
+        const double g0 = SC[sp], g1 = SB[sp];
         double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
-        if (active) {
+        if (gcur.active) {
           s00 = qd_el[0 * P3 + pt];
           s01 = qd_el[1 * P3 + pt];
           s02 = qd_el[2 * P3 + pt];
@@ -197,74 +257,78 @@ __global__ void __launch_bounds__(T::NT)
           s12 = qd_el[4 * P3 + pt];
           s22 = qd_el[5 * P3 + pt];
         }
-        if (active_slot) {
-          SA[sp] = s00 * g0 + s01 * g1 + s02 * g2;
-          SB[sp] = s01 * g0 + s11 * g1 + s12 * g2;
-        }
+        const double v0 = s00 * g0 + s01 * g1 + s02 * g2;
+        const double v1 = s01 * g0 + s11 * g1 + s12 * g2;
         v2[k] = s02 * g0 + s12 * g1 + s22 * g2;
+        if (active_slot) {
+          SC[sp] = v0;
+          SB[sp] = v1;
+        }
+        // p.(A p) over free nodes = sum_e u_e^T A_e u_e = sum_points grad u . S grad u
+        energy += g0 * v0 + g1 * v1 + g2 * v2[k];
       }
+      dot_acc += prm.coef * energy;
       if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
       __syncthreads();
-      // factors consumed: stream the next step's in while we transpose
+      // factors consumed: stream the next element's in while we finish this one
       if (c == NC - 1 && tid == 0 && step + G < nsteps && !(prm.ablate & 4)) issue_qdata(step + G);
 
-      // ---- transposed y-pencil (in place, slab B) and x-pencil (in place, slab A) ----
+      // ---- T: D^T along x (C, in place) and y (B, in place) ----
       if (active_slot) {
-        double col[P];
-#pragma unroll
-        for (int b = 0; b < P; ++b) col[b] = SB[lb * PL + b * RS + la];
-#pragma unroll
-        for (int o = 0; o < P; ++o) {
-          double s = 0.0;
-#pragma unroll
-          for (int b = 0; b < P; ++b) s += mats.D[b * P + o] * col[b];
-          SB[lb * PL + o * RS + la] = s;
-        }
-        double row[P];
-        double* rp = SA + lb * PL + la * RS;
+        double row[P], col[P];
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(rp + a);
+          const double2 v = *reinterpret_cast<const double2*>(SC + T::chunk(lb, la, a / 2));
           row[a] = v.x;
           row[a + 1] = v.y;
         }
-        if (P & 1) row[P - 1] = rp[P - 1];
-        double t[P];
+        if (P & 1) row[P - 1] = SC[T::off(lb, la, P - 1)];
+#pragma unroll
+        for (int b = 0; b < P; ++b) col[b] = SB[T::off(lb, b, la)];
+        double tx[P];
 #pragma unroll
         for (int o = 0; o < P; ++o) {
-          double s = 0.0;
+          double d[P];
+          load_row<P>(sDT + o * DR, d);
+          double sx = 0.0, sy = 0.0;
 #pragma unroll
-          for (int a = 0; a < P; ++a) s += mats.D[a * P + o] * row[a];
-          t[o] = s;
+          for (int a = 0; a < P; ++a) {
+            sx += d[a] * row[a];
+            sy += d[a] * col[a];
+          }
+          tx[o] = sx;
+          SB[T::off(lb, o, la)] = sy;
         }
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2)
-          *reinterpret_cast<double2*>(rp + a) = make_double2(t[a], t[a + 1]);
-        if (P & 1) rp[P - 1] = t[P - 1];
+          *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(tx[a], tx[a + 1]);
+        if (P & 1) SC[T::off(lb, la, P - 1)] = tx[P - 1];
       }
       __syncthreads();
 
-      // ---- z^T from registers + combine, G^T scatter ----
-      if (active) {
+      // ---- Z: D^T along z from registers + combine, G^T scatter ----
+      if (gcur.active) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {
+          double d[P];
+          load_row<P>(sDT + k * DR, d);
           double s = 0.0;
 #pragma unroll
-          for (int cc = 0; cc < P; ++cc) s += mats.D[cc * P + k] * v2[cc];
-          const int sp = k * PL + lb * RS + la;
-          const double yk = prm.coef * (SA[sp] + SB[sp] + s);
-          const int64_t node = node_at(k);
+          for (int cc = 0; cc < P; ++cc) s += d[cc] * v2[cc];
+          const int sp = T::off(k, lb, la);
+          const double yk = prm.coef * (SC[sp] + SB[sp] + s);
+          const int64_t node = node_of(gcur, k);
           if (prm.ablate & 2) {
-            dot_acc += u[k] * yk;
-          } else if (is_cons(node, k)) {
+          } else if ((gcur.cmask >> k) & 1u) {
             yc[node] = __ldg(xc + node);
           } else {
             red_add(yc + node, yk);
-            dot_acc += u[k] * yk;
           }
         }
       }
+      __syncthreads();  // B and C free for the next item's phase F
     }
+    gcur = geometry(step + G);
   }
 
   if (prm.dot_partials) {
