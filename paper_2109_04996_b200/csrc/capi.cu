@@ -229,7 +229,7 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
 // dot_part: per-CTA partials of x_free . y (fused p.Ap), *nparts set.
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
                   int* nparts, const int* stop, bool zero_y = true) {
-  if (zero_y) ck(cudaMemsetAsync(y, 0, sizeof(double) * op->size(), s), "cudaMemsetAsync");
+  if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask), "init_y");
   OpParams prm{};
   prm.x = x;
   prm.y = y;

@@ -62,6 +62,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk prefetch of a global range into L2 (bytes % 16 == 0, 16B aligned).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Generic-proxy smem writes must be ordered before a later async-proxy (bulk
 // copy) write into the same buffer.
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -18,8 +18,9 @@
 //     single bulk async copy (TMA engine, L2 evict_first) tracked by an
 //     mbarrier, double-buffered, while the current step computes;
 //   * G is computed from the structured-box lattice (or an int32 table for a
-//     general mesh); G^T is an FP64 RED into y (zeroed by the caller), and
-//     constrained nodes are written y = x directly (operator.cpp:141-143);
+//     general mesh); G^T is an FP64 RED into y, which the caller presets to
+//     y = x on constrained nodes and 0 elsewhere (operator.cpp:87-90,141-143),
+//     so constrained nodes are skipped here;
 //   * optionally, the partial p.(Ap) over unconstrained nodes is reduced per
 //     CTA (the first PCG dot, pcg.cpp:74, fused).
 //
@@ -388,9 +389,8 @@ __global__ void __launch_bounds__(T::NT)
         for (int k = 0; k < P; ++k) {
           bool cons;
           const int64_t node = node_of(qi, qj, k, cons);
-          if (cons) {
-            yc[node] = __ldg(xc + node);
-          } else {
+          // constrained rows: y = x is preset by the caller (init_y / PCG kernels)
+          if (!cons) {
             const double yk = prm.coef * yv[k];  // y += coef * (...)  (operator.cpp:131-135)
             red_add(yc + node, yk);
             dot_acc += u[k] * yk;

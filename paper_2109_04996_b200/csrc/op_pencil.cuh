@@ -118,18 +118,27 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   const int64_t G = gridDim.x;
   const int64_t NXY = prm.NX * prm.NY;
   uint64_t policy = 0;
-  auto issue_qdata = [&](int64_t s) {
+  auto qbytes = [&](int64_t s) -> uint32_t {
     const int64_t e0 = s * EPB;
     const int ne = (int)((prm.E - e0) < EPB ? (prm.E - e0) : EPB);
-    const uint32_t bytes = (uint32_t)(ne * T::QDS * 8);
+    return (uint32_t)(ne * T::QDS * 8);
+  };
+  auto issue_qdata = [&](int64_t s) {
+    const uint32_t bytes = qbytes(s);
     mbar_arrive_expect_tx(&qbar, bytes);
-    bulk_g2s(sQD, prm.qd + e0 * T::QDS, bytes, &qbar, policy);
+    bulk_g2s(sQD, prm.qd + s * EPB * T::QDS, bytes, &qbar, policy);
+  };
+  // the element after next: pull its factors HBM -> L2 now (no shared memory
+  // needed), so the later bulk copy into shared memory is an L2 hit
+  auto prefetch_qdata = [&](int64_t s) {
+    if (s < nsteps && !(prm.ablate & 8)) bulk_prefetch_l2(prm.qd + s * EPB * T::QDS, qbytes(s));
   };
   if (tid == 0) {
     mbar_init(&qbar, 1);
     fence_mbar_init();
     policy = l2_evict_first_policy();
     if ((int64_t)blockIdx.x < nsteps && !(prm.ablate & 4)) issue_qdata(blockIdx.x);
+    prefetch_qdata(blockIdx.x + G);
   }
 
   auto node_of = [&](const PencilGeo& g, int k) -> int64_t {
@@ -193,7 +202,6 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
 #pragma unroll 1
     for (int c = 0; c < NC; ++c, ++q) {
       double* yc = prm.y + c * prm.n_L;
-      const double* xc = prm.x + c * prm.n_L;
 
       // ---- F: D along x (-> C) and y (-> B) from slab A, one D row per two pencils ----
       if (active_slot) {
@@ -271,7 +279,10 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
       __syncthreads();
       // factors consumed: stream the next element's in while we finish this one
-      if (c == NC - 1 && tid == 0 && step + G < nsteps && !(prm.ablate & 4)) issue_qdata(step + G);
+      if (c == NC - 1 && tid == 0 && step + G < nsteps && !(prm.ablate & 4)) {
+        issue_qdata(step + G);
+        prefetch_qdata(step + 2 * G);
+      }
 
       // ---- T: D^T along x (C, in place) and y (B, in place) ----
       if (active_slot) {
@@ -318,12 +329,8 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
           const int sp = T::off(k, lb, la);
           const double yk = prm.coef * (SC[sp] + SB[sp] + s);
           const int64_t node = node_of(gcur, k);
-          if (prm.ablate & 2) {
-          } else if ((gcur.cmask >> k) & 1u) {
-            yc[node] = __ldg(xc + node);
-          } else {
-            red_add(yc + node, yk);
-          }
+          // constrained rows (y = x) are preset by the caller
+          if (!(prm.ablate & 2) && !((gcur.cmask >> k) & 1u)) red_add(yc + node, yk);
         }
       }
       __syncthreads();  // B and C free for the next item's phase F

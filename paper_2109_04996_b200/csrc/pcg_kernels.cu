@@ -45,13 +45,14 @@ __global__ void __launch_bounds__(VT)
       const int64_t i = c * n_L + node;
       const double bi = b[i];
       const double zi = d ? bi / d[i] : bi;
+      const bool cons = is_cons(cons_mask, node);
       x[i] = 0.0;
       r[i] = bi;
       p[i] = zi;
-      Ap[i] = 0.0;
+      Ap[i] = cons ? zi : 0.0;  // operator kernels skip constrained rows (A p = p there)
       rr += bi * bi;
       rz += bi * zi;
-      if (is_cons(cons_mask, node)) cc += zi * zi;
+      if (cons) cc += zi * zi;
     }
   }
   const double s0 = block_sum<VT>(rr, scratch);
@@ -187,9 +188,10 @@ __global__ void __launch_bounds__(VT)
       const int64_t i = c * n_L + node;
       const double zi = d ? r[i] / d[i] : r[i];
       const double pi = zi + beta * p[i];
+      const bool cons = is_cons(cons_mask, node);
       p[i] = pi;
-      Ap[i] = 0.0;
-      if (is_cons(cons_mask, node)) cc += pi * pi;
+      Ap[i] = cons ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
+      if (cons) cc += pi * pi;
     }
   }
   if (cons_mask) {
@@ -206,6 +208,19 @@ __global__ void __launch_bounds__(VT)
   if (threadIdx.x == 0) st->cons_pp = s;
 }
 
+// y = x on constrained rows, 0 elsewhere: the RED target of an operator apply
+// (operator.cpp:87-90,141-143).
+__global__ void __launch_bounds__(VT)
+    init_y_kernel(int64_t n_L, int m, const double* __restrict__ x, double* __restrict__ y,
+                  const uint32_t* cons_mask) {
+  const int64_t stride = (int64_t)gridDim.x * VT;
+  for (int c = 0; c < m; ++c)
+    for (int64_t node = (int64_t)blockIdx.x * VT + threadIdx.x; node < n_L; node += stride) {
+      const int64_t i = c * n_L + node;
+      y[i] = is_cons(cons_mask, node) ? x[i] : 0.0;
+    }
+}
+
 // ------------------------------------------------------------------ host side
 int vec_grid() { return num_sms() * 4; }
 
@@ -216,6 +231,14 @@ cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b,
   pcg_init_kernel<<<g, VT, 0, s>>>(n_L, m, b, d, x, r, p, Ap, mask, part);
   pcg_init_finalize<<<1, VT, 0, s>>>(st, part, g, hist);
   count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
+                          const uint32_t* mask) {
+  if (!mask) return cudaMemsetAsync(y, 0, sizeof(double) * n_L * m, s);
+  init_y_kernel<<<vec_grid(), VT, 0, s>>>(n_L, m, x, y, mask);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -13,6 +13,8 @@ struct PcgState {
 };
 
 int vec_grid();
+cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
+                          const uint32_t* mask);
 cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b, const double* d,
                             double* x, double* r, double* p, double* Ap, const uint32_t* mask,
                             double* part, PcgState* st, double* hist);
