@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   // the element after next: pull its factors HBM -> L2 now (no shared memory
   // needed), so the later bulk copy into shared memory is an L2 hit
   auto prefetch_qdata = [&](int64_t s) {
-    if (s < nsteps && !(prm.ablate & 8)) bulk_prefetch_l2(prm.qd + s * EPB * T::QDS, qbytes(s));
+    if (s < nsteps && (prm.ablate & 8)) bulk_prefetch_l2(prm.qd + s * EPB * T::QDS, qbytes(s));
   };
   if (tid == 0) {
     mbar_init(&qbar, 1);

@@ -1,18 +1,23 @@
-// K2-K4: device-resident Jacobi-PCG vector phases and fixed-order reductions.
+// Device-resident Jacobi-PCG: vector phases and fixed-order reductions.
 //
-// Restates the reference recurrence (proj/src/pcg.cpp:24-115) with the
-// scalars kept on the device (PcgState) so a whole solve runs without a host
-// round trip per iteration:
-//   init     x = 0, r = b, p = z = b/d, partials of b.b and b.z
-//   K1       Ap = A p (op_kernel.cuh) + partials of p.Ap over free nodes
-//   alpha    pAp = sum(partials) + sum_{constrained} p^2; checks; alpha
-//   update   x += alpha p, r -= alpha Ap; partials of r.r and r.(r/d)
-//   resid    ||r||, history, convergence / limit; beta = rho'/rho
-//   dir      p = r/d + beta p; Ap = 0 (next RED target); partials of p^2 on
-//            constrained nodes
-// Every reduction is per-CTA partials (fixed grid) summed in a fixed order by
-// one block: bitwise reproducible run to run for a fixed launch geometry
-// (the reference's dot_deterministic, parallel.cpp:69-106, plays that role).
+// Restates the reference recurrence (proj/src/pcg.cpp:24-115) with every
+// scalar kept on the device, three launches per iteration:
+//   K1      Ap += A p over free rows (op_pencil.cuh / op_kernel.cuh) and
+//           per-CTA partials of p.(A p)
+//   update  [prologue] pAp = sum(K1 partials) + sum_{constrained} p^2, the
+//           reference's checks (pcg.cpp:74-82), alpha = rho / pAp;
+//           x += alpha p, r -= alpha Ap; partials of r.r and r.(r/d)
+//   dir     [prologue] ||r||, history, convergence / limit (pcg.cpp:90-99),
+//           beta = rho' / rho; p = r/d + beta p; Ap = (constrained ? p : 0),
+//           the next RED target; partials of p^2 on constrained rows
+// The prologues are computed REDUNDANTLY by every block from the same
+// partials in the same fixed order, so all blocks agree on alpha / beta /
+// stop without a separate finalize launch; block 0 publishes them.  Scalars
+// a block reads at its start and the previous kernel wrote (rho) are
+// double-buffered by iteration parity; the iteration index is a kernel
+// argument.  Every reduction is per-CTA partials over a fixed grid summed in
+// a fixed order: bitwise reproducible run to run (the reference's
+// dot_deterministic, parallel.cpp:69-106, plays that role).
 #include "hxf_device.cuh"
 #include "pcg_kernels.h"
 
@@ -25,11 +30,16 @@ __device__ __forceinline__ bool is_cons(const uint32_t* mask, int64_t node) {
   return mask && ((mask[node >> 5] >> (node & 31)) & 1u);
 }
 
-// Fixed-order sum of `n` partials with stride `stride`, one block of VT threads.
-__device__ double reduce_partials(const double* part, int n, double* scratch) {
+// Fixed-order sum of n partials by one block; result broadcast to all threads.
+__device__ double block_reduce_all(const double* part, int n, double* scratch) {
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += VT) s += part[i];
-  return block_sum<VT>(s, scratch);  // valid on thread 0
+  s = block_sum<VT>(s, scratch);
+  if (threadIdx.x == 0) scratch[0] = s;
+  __syncthreads();
+  const double r = scratch[0];
+  __syncthreads();
+  return r;
 }
 }  // namespace
 
@@ -66,18 +76,18 @@ __global__ void __launch_bounds__(VT)
 }
 
 __global__ void __launch_bounds__(VT)
-    pcg_init_finalize(PcgState* st, const double* part, int g, double* hist) {
+    pcg_init_finalize(PcgState* st, const double* part, int g, double* hist, double* cons_part) {
   __shared__ double scratch[VT / 32];
-  const double rr = reduce_partials(part, g, scratch);
-  const double rz = reduce_partials(part + g, g, scratch);
-  const double cc = reduce_partials(part + 2 * g, g, scratch);
+  const double rr = block_reduce_all(part, g, scratch);
+  const double rz = block_reduce_all(part + g, g, scratch);
+  const double cc = block_reduce_all(part + 2 * g, g, scratch);
   if (threadIdx.x == 0) {
+    cons_part[0] = cc;  // read by the first update kernel as a 1-entry partial list
     const double norm_b = sqrt(rr);
     st->it = 0;
     st->converged = 0;
     st->error = 0;
     st->stop = 0;
-    st->cons_pp = cc;
     if (!isfinite(norm_b)) {
       st->error = PCG_ERR_RHS;
       st->stop = 1;
@@ -92,43 +102,36 @@ __global__ void __launch_bounds__(VT)
       st->stop = 1;
       return;
     }
-    st->rho = rz;
+    st->rho[1] = rz;  // rho before iteration 1
   }
 }
 
+// Iteration `it` (1-based): alpha prologue + x/r update + r.r, r.z partials.
 __global__ void __launch_bounds__(VT)
-    pcg_alpha_finalize(PcgState* st, const double* kpart, int gk) {
-  __shared__ double scratch[VT / 32];
-  if (st->stop) return;
-  const double s = reduce_partials(kpart, gk, scratch);
-  if (threadIdx.x == 0) {
-    const double pap = s + st->cons_pp;
-    st->pap = pap;
-    if (!isfinite(pap)) {
-      st->error = PCG_ERR_APPLY_NAN;
-      st->stop = 1;
-      return;
-    }
-    if (pap <= 0.0) {
-      if (st->rho == 0.0) {
-        st->converged = 1;
-      } else {
-        st->error = PCG_ERR_INDEFINITE;
-      }
-      st->stop = 1;
-      return;
-    }
-    st->alpha = st->rho / pap;
-  }
-}
-
-__global__ void __launch_bounds__(VT)
-    pcg_update_kernel(const PcgState* st, int64_t n, const double* __restrict__ d,
-                      double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+    pcg_update_kernel(PcgState* st, int it, const double* kpart, int gk, const double* cpart,
+                      int gc, int64_t n, const double* __restrict__ d, double* __restrict__ x,
+                      double* __restrict__ r, const double* __restrict__ p,
                       const double* __restrict__ Ap, double* part) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double alpha = st->alpha;
+  const double pap = block_reduce_all(kpart, gk, scratch) + block_reduce_all(cpart, gc, scratch);
+  const double rho = st->rho[it & 1];
+  // pcg.cpp:74-82
+  if (!isfinite(pap) || pap <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pap = pap;
+      if (!isfinite(pap)) st->error = PCG_ERR_APPLY_NAN;
+      else if (rho == 0.0) st->converged = 1;
+      else st->error = PCG_ERR_INDEFINITE;
+      st->stop = 1;
+    }
+    return;
+  }
+  const double alpha = rho / pap;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->pap = pap;
+    st->alpha = alpha;
+  }
   double rr = 0.0, rz = 0.0;
   const int64_t stride = (int64_t)gridDim.x * VT;
   for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += stride) {
@@ -146,41 +149,39 @@ __global__ void __launch_bounds__(VT)
   }
 }
 
+// Iteration `it`: residual / convergence prologue + p = z + beta p, Ap preset.
 __global__ void __launch_bounds__(VT)
-    pcg_update_finalize(PcgState* st, const double* part, int g, double* hist) {
-  __shared__ double scratch[VT / 32];
-  if (st->stop) return;
-  const double rr = reduce_partials(part, g, scratch);
-  const double rz = reduce_partials(part + g, g, scratch);
-  if (threadIdx.x == 0) {
-    const double res = sqrt(rr);
-    if (!isfinite(res)) {
-      st->error = PCG_ERR_RESID;
-      st->stop = 1;
-      return;
-    }
-    const int it = st->it + 1;
-    st->it = it;
-    st->res = res;
-    hist[it] = res;
-    if (res <= st->target) {
-      st->converged = 1;
-      if (!st->fixed) st->stop = 1;
-    }
-    if (it == st->limit || res == 0.0) st->stop = 1;
-    if (st->stop) return;
-    st->beta = rz / st->rho;
-    st->rho = rz;
-  }
-}
-
-__global__ void __launch_bounds__(VT)
-    pcg_direction_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ d,
+    pcg_direction_kernel(PcgState* st, int it, const double* upart, int gu, double* hist,
+                         int64_t n_L, int m, const double* __restrict__ d,
                          const double* __restrict__ r, double* __restrict__ p,
-                         double* __restrict__ Ap, const uint32_t* cons_mask, double* part) {
+                         double* __restrict__ Ap, const uint32_t* cons_mask, double* cpart) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double beta = st->beta;
+  const double rr = block_reduce_all(upart, gu, scratch);
+  const double rz = block_reduce_all(upart + gu, gu, scratch);
+  const double res = sqrt(rr);
+  const double rho = st->rho[it & 1];
+  // pcg.cpp:90-107
+  const bool bad = !isfinite(res);
+  const bool conv = res <= st->target;
+  const bool stop = bad || (conv && !st->fixed) || it == st->limit || res == 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bad) {
+      st->error = PCG_ERR_RESID;
+    } else {
+      st->it = it;
+      st->res = res;
+      hist[it] = res;
+      if (conv) st->converged = 1;
+    }
+    if (!stop) {
+      st->beta = rz / rho;
+      st->rho[(it + 1) & 1] = rz;
+    }
+    st->stop = stop ? 1 : 0;
+  }
+  if (stop) return;
+  const double beta = rz / rho;
   double cc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * VT;
   for (int c = 0; c < m; ++c) {
@@ -194,18 +195,8 @@ __global__ void __launch_bounds__(VT)
       if (cons) cc += pi * pi;
     }
   }
-  if (cons_mask) {
-    const double s = block_sum<VT>(cc, scratch);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
-  }
-}
-
-__global__ void __launch_bounds__(VT)
-    pcg_cons_finalize(PcgState* st, const double* part, int g) {
-  __shared__ double scratch[VT / 32];
-  if (st->stop) return;
-  const double s = reduce_partials(part, g, scratch);
-  if (threadIdx.x == 0) st->cons_pp = s;
+  const double s = block_sum<VT>(cc, scratch);
+  if (threadIdx.x == 0) cpart[blockIdx.x] = s;
 }
 
 // y = x on constrained rows, 0 elsewhere: the RED target of an operator apply
@@ -224,16 +215,6 @@ __global__ void __launch_bounds__(VT)
 // ------------------------------------------------------------------ host side
 int vec_grid() { return num_sms() * 4; }
 
-cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b, const double* d,
-                            double* x, double* r, double* p, double* Ap, const uint32_t* mask,
-                            double* part, PcgState* st, double* hist) {
-  const int g = vec_grid();
-  pcg_init_kernel<<<g, VT, 0, s>>>(n_L, m, b, d, x, r, p, Ap, mask, part);
-  pcg_init_finalize<<<1, VT, 0, s>>>(st, part, g, hist);
-  count_launch(2);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
                           const uint32_t* mask) {
   if (!mask) return cudaMemsetAsync(y, 0, sizeof(double) * n_L * m, s);
@@ -242,32 +223,32 @@ cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, d
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_alpha(cudaStream_t s, PcgState* st, const double* kpart, int gk) {
-  pcg_alpha_finalize<<<1, VT, 0, s>>>(st, kpart, gk);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int64_t n, const double* d, double* x,
-                              double* r, const double* p, const double* Ap, double* part,
-                              double* hist) {
+cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b, const double* d,
+                            double* x, double* r, double* p, double* Ap, const uint32_t* mask,
+                            double* part, PcgState* st, double* hist, double* cons_part) {
   const int g = vec_grid();
-  pcg_update_kernel<<<g, VT, 0, s>>>(st, n, d, x, r, p, Ap, part);
-  pcg_update_finalize<<<1, VT, 0, s>>>(st, part, g, hist);
+  pcg_init_kernel<<<g, VT, 0, s>>>(n_L, m, b, d, x, r, p, Ap, mask, part);
+  pcg_init_finalize<<<1, VT, 0, s>>>(st, part, g, hist, cons_part);
   count_launch(2);
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int64_t n_L, int m,
-                                 const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, double* part) {
-  const int g = vec_grid();
-  pcg_direction_kernel<<<g, VT, 0, s>>>(st, n_L, m, d, r, p, Ap, mask, part);
+cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, const double* kpart, int gk,
+                              const double* cpart, int gc, int64_t n, const double* d, double* x,
+                              double* r, const double* p, const double* Ap, double* upart) {
+  pcg_update_kernel<<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r, p, Ap,
+                                             upart);
   count_launch();
-  if (mask) {
-    pcg_cons_finalize<<<1, VT, 0, s>>>(st, part, g);
-    count_launch();
-  }
+  return cudaGetLastError();
+}
+
+cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, const double* upart,
+                                 double* hist, int64_t n_L, int m, const double* d,
+                                 const double* r, double* p, double* Ap, const uint32_t* mask,
+                                 double* cpart) {
+  pcg_direction_kernel<<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m, d, r, p,
+                                                Ap, mask, cpart);
+  count_launch();
   return cudaGetLastError();
 }
 
