@@ -824,12 +824,16 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     const int* stop = &op->d_state->stop;
 
     // one iteration: K1 (fused operator + p.Ap partials), update, direction
+    // (External: inside a captured graph the record is a real timing event)
+    auto record = [&](cudaEvent_t e) {
+      ck(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal), "event");
+    };
     auto iteration = [&](int it) {
       int nparts = 0;
-      ck(cudaEventRecord(op->ev[2 * (it - 1)], s), "event");
+      record(op->ev[2 * (it - 1)]);
       // Ap was preset by the init / direction kernel: no memset pass here
       device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false);
-      ck(cudaEventRecord(op->ev[2 * (it - 1) + 1], s), "event");
+      record(op->ev[2 * (it - 1) + 1]);
       ck(pcg_launch_update(s, op->d_state, it, op->d_part, nparts, cpart, it == 1 ? 1 : vg,
                            int64_t(n), dd, dx, r, p, Ap, upart),
          "pcg update");
