@@ -825,8 +825,11 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
 
     // one iteration: K1 (fused operator + p.Ap partials), update, direction
     // (External: inside a captured graph the record is a real timing event)
+    bool capturing = false;
     auto record = [&](cudaEvent_t e) {
-      ck(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal), "event");
+      ck(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                   : cudaEventRecord(e, s),
+         "event");
     };
     auto iteration = [&](int it) {
       int nparts = 0;
@@ -860,8 +863,10 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
         const int64_t before = hxf_launch_count();
         cudaGraph_t graph;
         ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "capture");
+        capturing = true;
         init();
         for (int it = 1; it <= limit; ++it) iteration(it);
+        capturing = false;
         ck(cudaStreamEndCapture(s, &graph), "capture");
         ck(cudaGraphInstantiate(&op->graph_exec, graph, 0), "graph instantiate");
         cudaGraphDestroy(graph);
