@@ -278,3 +278,62 @@ def rel_max_diff(a, b) -> float:
     scale = float(np.max(np.abs(a))) if a.size else 0.0
     diff = float(np.max(np.abs(a - b))) if a.size else 0.0
     return diff / scale if scale > 0 else diff
+
+
+class RefWithBackend:
+    """A reference BpProblem (oracle/_ref) driven both by the reference (CPU)
+    and by the reference-side integration integration/hexfem_hxf.cpp (GPU).
+    which = 0 reference, 1 hxf backend."""
+
+    def __init__(self, bp: str, degree: int, dims, deform: str = "none", threads: int = 2):
+        path = HERE / "_ref" / "libref_hxf.so"
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (make -C oracle ref after the product)")
+        L = C.CDLL(str(path))
+        P, I, D = C.c_void_p, C.c_int, C.c_double
+        pd, pi = C.POINTER(C.c_double), C.POINTER(C.c_int)
+        L.orh_last_error.restype = C.c_char_p
+        L.orh_setup.restype = P
+        L.orh_setup.argtypes = [I, I, I, I, I, I, I]
+        L.orh_free.argtypes = [P]
+        L.orh_size.restype = C.c_int64
+        L.orh_size.argtypes = [P]
+        L.orh_apply.argtypes = [P, I, pd, pd]
+        L.orh_diagonal.argtypes = [P, I, pd]
+        L.orh_solve.argtypes = [P, I, D, I, pd, pi, pi]
+        self._L = L
+        dims = tuple(int(d) for d in dims)
+        h = L.orh_setup(BP_IDS[bp], degree, dims[0], dims[1], dims[2],
+                        1 if deform == "sine" else 0, threads)
+        if not h:
+            raise ValueError(L.orh_last_error().decode())
+        self._h = C.c_void_p(h)
+        self.size = int(L.orh_size(self._h))
+
+    def _ck(self, rc):
+        if rc:
+            raise (ValueError if rc == 1 else RuntimeError)(self._L.orh_last_error().decode())
+
+    def apply(self, x, which):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.size)
+        self._ck(self._L.orh_apply(self._h, which, _dp(x), _dp(y)))
+        return y
+
+    def diagonal(self, which):
+        d = np.zeros(self.size)
+        self._ck(self._L.orh_diagonal(self._h, which, _dp(d)))
+        return d
+
+    def solve(self, which, tol=1e-8, jacobi=True):
+        x = np.zeros(self.size)
+        it, conv = C.c_int(0), C.c_int(0)
+        self._ck(self._L.orh_solve(self._h, which, tol, int(jacobi), _dp(x), C.byref(it),
+                                   C.byref(conv)))
+        return x, it.value, bool(conv.value)
+
+    def __del__(self):
+        try:
+            self._L.orh_free(self._h)
+        except Exception:
+            pass
