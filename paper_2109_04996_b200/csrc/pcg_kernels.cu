@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(VT)
 }
 
 // Iteration `it` (1-based): alpha prologue + x/r update + r.r, r.z partials.
+// VEC: all vectors 16-byte aligned -> two entries per 128-bit access, two
+// pairs per loop trip (more bytes in flight per thread).
+template <bool VEC>
 __global__ void __launch_bounds__(VT)
     pcg_update_kernel(PcgState* st, int it, const double* kpart, int gk, const double* cpart,
                       int gc, int64_t n, const double* __restrict__ d, double* __restrict__ x,
@@ -133,13 +136,45 @@ __global__ void __launch_bounds__(VT)
     st->alpha = alpha;
   }
   double rr = 0.0, rz = 0.0;
+  const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
-  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += stride) {
+  auto one = [&](int64_t i) {
     x[i] += alpha * p[i];
     const double ri = r[i] - alpha * Ap[i];
     r[i] = ri;
     rr += ri * ri;
     rz += ri * (d ? ri / d[i] : ri);
+  };
+  if constexpr (VEC) {
+    const int64_t n2 = n / 2;
+    auto two = [&](int64_t k, double2 xv, double2 pv, double2 rv, double2 av, double2 dv) {
+      xv.x += alpha * pv.x;
+      xv.y += alpha * pv.y;
+      rv.x -= alpha * av.x;
+      rv.y -= alpha * av.y;
+      reinterpret_cast<double2*>(x)[k] = xv;
+      reinterpret_cast<double2*>(r)[k] = rv;
+      rr += rv.x * rv.x + rv.y * rv.y;
+      rz += rv.x * (d ? rv.x / dv.x : rv.x) + rv.y * (d ? rv.y / dv.y : rv.y);
+    };
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const double2* a2 = reinterpret_cast<const double2*>(Ap);
+    const double2* d2 = reinterpret_cast<const double2*>(d);
+    const double2 one2 = make_double2(1.0, 1.0);
+    int64_t k = tid;
+    for (; k + stride < n2; k += 2 * stride) {
+      const int64_t k1 = k + stride;
+      const double2 xa = x2[k], pa = p2[k], ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
+      const double2 xb = x2[k1], pb = p2[k1], rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
+      two(k, xa, pa, ra, aa, da);
+      two(k1, xb, pb, rb, ab, db);
+    }
+    if (k < n2) two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
+    if ((n & 1) && tid == 0) one(n - 1);
+  } else {
+    for (int64_t i = tid; i < n; i += stride) one(i);
   }
   const double s0 = block_sum<VT>(rr, scratch);
   const double s1 = block_sum<VT>(rz, scratch);
@@ -150,6 +185,8 @@ __global__ void __launch_bounds__(VT)
 }
 
 // Iteration `it`: residual / convergence prologue + p = z + beta p, Ap preset.
+// VEC: 16-byte aligned vectors and an even component stride n_L.
+template <bool VEC>
 __global__ void __launch_bounds__(VT)
     pcg_direction_kernel(PcgState* st, int it, const double* upart, int gu, double* hist,
                          int64_t n_L, int m, const double* __restrict__ d,
@@ -183,16 +220,39 @@ __global__ void __launch_bounds__(VT)
   if (stop) return;
   const double beta = rz / rho;
   double cc = 0.0;
+  const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
   for (int c = 0; c < m; ++c) {
-    for (int64_t node = (int64_t)blockIdx.x * VT + threadIdx.x; node < n_L; node += stride) {
-      const int64_t i = c * n_L + node;
-      const double zi = d ? r[i] / d[i] : r[i];
-      const double pi = zi + beta * p[i];
-      const bool cons = is_cons(cons_mask, node);
-      p[i] = pi;
-      Ap[i] = cons ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
-      if (cons) cc += pi * pi;
+    const int64_t o = c * n_L;
+    if constexpr (VEC) {
+      const int64_t h = n_L / 2;  // n_L even
+      const double2* r2 = reinterpret_cast<const double2*>(r + o);
+      const double2* d2 = reinterpret_cast<const double2*>(d + o);
+      double2* p2 = reinterpret_cast<double2*>(p + o);
+      double2* a2 = reinterpret_cast<double2*>(Ap + o);
+      for (int64_t k = tid; k < h; k += stride) {
+        const double2 rv = r2[k], pv = p2[k];
+        const double2 dv = d ? d2[k] : make_double2(1.0, 1.0);
+        double2 q;
+        q.x = (d ? rv.x / dv.x : rv.x) + beta * pv.x;
+        q.y = (d ? rv.y / dv.y : rv.y) + beta * pv.y;
+        p2[k] = q;
+        const int64_t node = 2 * k;
+        const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
+        a2[k] = make_double2((w & 1u) ? q.x : 0.0, (w & 2u) ? q.y : 0.0);
+        if (w & 1u) cc += q.x * q.x;
+        if (w & 2u) cc += q.y * q.y;
+      }
+    } else {
+      for (int64_t node = tid; node < n_L; node += stride) {
+        const int64_t i = o + node;
+        const double zi = d ? r[i] / d[i] : r[i];
+        const double pi = zi + beta * p[i];
+        const bool cons = is_cons(cons_mask, node);
+        p[i] = pi;
+        Ap[i] = cons ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
+        if (cons) cc += pi * pi;
+      }
     }
   }
   const double s = block_sum<VT>(cc, scratch);
@@ -213,7 +273,11 @@ __global__ void __launch_bounds__(VT)
 }
 
 // ------------------------------------------------------------------ host side
-int vec_grid() { return num_sms() * 4; }
+int vec_grid() { return num_sms() * 8; }
+
+namespace {
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+}  // namespace
 
 cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
                           const uint32_t* mask) {
@@ -236,8 +300,12 @@ cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b,
 cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, const double* kpart, int gk,
                               const double* cpart, int gc, int64_t n, const double* d, double* x,
                               double* r, const double* p, const double* Ap, double* upart) {
-  pcg_update_kernel<<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r, p, Ap,
-                                             upart);
+  if (aligned16(d) && aligned16(x) && aligned16(r) && aligned16(p) && aligned16(Ap))
+    pcg_update_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r, p,
+                                                     Ap, upart);
+  else
+    pcg_update_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r,
+                                                      p, Ap, upart);
   count_launch();
   return cudaGetLastError();
 }
@@ -246,8 +314,12 @@ cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, const dou
                                  double* hist, int64_t n_L, int m, const double* d,
                                  const double* r, double* p, double* Ap, const uint32_t* mask,
                                  double* cpart) {
-  pcg_direction_kernel<<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m, d, r, p,
-                                                Ap, mask, cpart);
+  if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
+    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m,
+                                                        d, r, p, Ap, mask, cpart);
+  else
+    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m,
+                                                         d, r, p, Ap, mask, cpart);
   count_launch();
   return cudaGetLastError();
 }
