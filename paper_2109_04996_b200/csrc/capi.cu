@@ -229,10 +229,11 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
   return stream ? static_cast<cudaStream_t>(stream) : op->ctx->stream;
 }
 
-// y = op x on the device (y zeroed here; the kernel REDs into it).
-// dot_part: per-CTA partials of x_free . y (fused p.Ap), *nparts set.
+// y = op x on the device (y preset here unless zero_y is false; the kernel
+// REDs into it).  PCG (st != nullptr): per-CTA partials of p.(A p) go to
+// dot_part and the last CTA of the last pass derives alpha into *st.
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
-                  int* nparts, const int* stop, bool zero_y = true) {
+                  int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr) {
   if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask), "init_y");
   OpParams prm{};
   prm.x = x;
@@ -250,6 +251,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.stop = stop;
   prm.ablate = ablate_bits();
   prm.D = op->d_G;
+  const int last_pass = op->beta != 0.0 ? 1 : 0;
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
     const double coef = pass == 0 ? op->alpha : op->beta;
@@ -257,6 +259,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
     prm.qd = pass == 0 ? op->d_qd_diff : op->d_qd_mass;
     prm.coef = coef;
     prm.dot_partials = dot_part ? dot_part + total : nullptr;
+    prm.fin = PcgAlphaFin{pass == last_pass ? st : nullptr, dot_part, total};
     int grid = 0;
     const cudaError_t err = launch_op(op->P, op->Q, op->m, op->interp, pass == 0 ? 1 : 2, prm,
                                       op->B.data(), op->Dq.data(), s, &grid);
@@ -813,9 +816,7 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     double* p = op->w_p.ensure(n);
     double* Ap = op->w_Ap.ensure(n);
     const int vg = vec_grid();
-    double* vpart = op->w_vpart.ensure(size_t(6 * vg));
-    double* upart = vpart + 3 * vg;   // r.r / r.z partials of the update kernel
-    double* cpart = vpart + 5 * vg;   // p^2 on constrained rows (direction kernel)
+    double* vpart = op->w_vpart.ensure(size_t(3 * vg));  // per-CTA partials (<= 3 per CTA)
     double* hist = op->w_hist.ensure(size_t(limit) + 2);
     PcgState st{};
     st.tol = opts->tol_rel;
@@ -823,7 +824,6 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     st.fixed = fixed ? 1 : 0;
     const int* stop = &op->d_state->stop;
 
-    // one iteration: K1 (fused operator + p.Ap partials), update, direction
     // (External: inside a captured graph the record is a real timing event)
     bool capturing = false;
     auto record = [&](cudaEvent_t e) {
@@ -831,22 +831,22 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
                    : cudaEventRecord(e, s),
          "event");
     };
+    // one iteration: K1 (fused operator, last CTA -> alpha), update (last
+    // CTA -> residual, beta, stop), direction (last CTA -> constrained p^2)
     auto iteration = [&](int it) {
       int nparts = 0;
       record(op->ev[2 * (it - 1)]);
       // Ap was preset by the init / direction kernel: no memset pass here
-      device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false);
+      device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state);
       record(op->ev[2 * (it - 1) + 1]);
-      ck(pcg_launch_update(s, op->d_state, it, op->d_part, nparts, cpart, it == 1 ? 1 : vg,
-                           int64_t(n), dd, dx, r, p, Ap, upart),
+      ck(pcg_launch_update(s, op->d_state, it, int64_t(n), dd, dx, r, p, Ap, vpart, hist),
          "pcg update");
-      ck(pcg_launch_direction(s, op->d_state, it, upart, hist, op->n_L, op->m, dd, r, p, Ap,
-                              op->d_mask, cpart),
+      ck(pcg_launch_direction(s, op->d_state, op->n_L, op->m, dd, r, p, Ap, op->d_mask, vpart),
          "pcg direction");
     };
     auto init = [&] {
-      ck(pcg_launch_init(s, op->n_L, op->m, db, dd, dx, r, p, Ap, op->d_mask, vpart, op->d_state,
-                         hist, cpart),
+      ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, db, dd, dx, r, p, Ap, op->d_mask, vpart,
+                         hist),
          "pcg init");
     };
 

@@ -10,6 +10,25 @@
 
 namespace hxf {
 
+enum PcgError { PCG_OK = 0, PCG_ERR_RHS = 1, PCG_ERR_APPLY_NAN = 2, PCG_ERR_INDEFINITE = 3,
+                PCG_ERR_RESID = 4 };
+
+// Device-resident PCG scalars (pcg_kernels.cu, pcg_device.cuh).
+struct PcgState {
+  double rho, pap, alpha, beta, norm_b, target, res, tol, cons_pp;
+  int it, stop, converged, error, limit, fixed;
+  unsigned int counter[4];  // last-block counters: K1, update, direction, init
+};
+
+// Last-CTA finalisation of p.(A p) inside the operator kernel (PCG only):
+// the CTA that finishes last sums every partial in a fixed order and derives
+// alpha (pcg.cpp:74-82), so no separate reduction launch is needed.
+struct PcgAlphaFin {
+  PcgState* st;         // nullptr: plain apply
+  const double* parts;  // all partials of this apply (earlier passes first)
+  int nparts;           // partials written by earlier passes (this launch adds gridDim.x)
+};
+
 // Arguments of the fused operator kernel (op_kernel.cuh).
 struct OpParams {
   const double* x;
@@ -26,6 +45,7 @@ struct OpParams {
   double coef;               // alpha (diffusion) or beta (mass)
   int ablate;                // measurement-only ablation bits (HXF_ABLATE), 0 in production
   const double* D;           // device copy of the 1-D derivative matrix (collocated path)
+  PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
 };
 
 // Launch the fused operator kernel instance for (P, Q, NC, interp, qk);

@@ -32,6 +32,7 @@
 #pragma once
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
+#include "pcg_device.cuh"
 
 namespace hxf {
 
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(T::NT)
   if (prm.dot_partials) {
     const double s = block_sum<NT>(dot_acc, red_scratch);
     if (tid == 0) prm.dot_partials[blockIdx.x] = s;
+    pcg_alpha_epilogue<NT>(prm.fin, red_scratch);
   }
 }
 

@@ -24,6 +24,7 @@
 #pragma once
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
+#include "pcg_device.cuh"
 
 namespace hxf {
 
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   if (prm.dot_partials) {
     const double s = block_sum<NT>(dot_acc, red_scratch);
     if (tid == 0) prm.dot_partials[blockIdx.x] = s;
+    pcg_alpha_epilogue<NT>(prm.fin, red_scratch);
   }
 }
 

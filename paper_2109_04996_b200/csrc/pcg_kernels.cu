@@ -2,23 +2,20 @@
 //
 // Restates the reference recurrence (proj/src/pcg.cpp:24-115) with every
 // scalar kept on the device, three launches per iteration:
-//   K1      Ap += A p over free rows (op_pencil.cuh / op_kernel.cuh) and
-//           per-CTA partials of p.(A p)
-//   update  [prologue] pAp = sum(K1 partials) + sum_{constrained} p^2, the
-//           reference's checks (pcg.cpp:74-82), alpha = rho / pAp;
-//           x += alpha p, r -= alpha Ap; partials of r.r and r.(r/d)
-//   dir     [prologue] ||r||, history, convergence / limit (pcg.cpp:90-99),
-//           beta = rho' / rho; p = r/d + beta p; Ap = (constrained ? p : 0),
-//           the next RED target; partials of p^2 on constrained rows
-// The prologues are computed REDUNDANTLY by every block from the same
-// partials in the same fixed order, so all blocks agree on alpha / beta /
-// stop without a separate finalize launch; block 0 publishes them.  Scalars
-// a block reads at its start and the previous kernel wrote (rho) are
-// double-buffered by iteration parity; the iteration index is a kernel
-// argument.  Every reduction is per-CTA partials over a fixed grid summed in
-// a fixed order: bitwise reproducible run to run (the reference's
-// dot_deterministic, parallel.cpp:69-106, plays that role).
-#include "hxf_device.cuh"
+//   K1      Ap += A p over free rows (op_pencil.cuh / op_kernel.cuh); its last
+//           CTA sums the p.(A p) partials + the constrained part and derives
+//           alpha with the reference's checks (pcg.cpp:74-82)
+//   update  x += alpha p, r -= alpha Ap; last CTA: ||r||, history,
+//           convergence / limit (pcg.cpp:90-99), beta = rho' / rho
+//   dir     p = r/d + beta p; Ap = (constrained ? p : 0), the next RED
+//           target; last CTA: sum of p^2 on constrained rows
+// Each reduction is per-CTA partials over a fixed grid summed in a fixed
+// order by the CTA that finishes last ("last CTA" pattern, pcg_device.cuh):
+// no extra launches, bitwise reproducible run to run (the reference's
+// dot_deterministic, parallel.cpp:69-106, plays that role).  A kernel reads
+// the stop flag only at its start; it is written only by a last CTA.
+
+#include "pcg_device.cuh"
 #include "pcg_kernels.h"
 
 namespace hxf {
@@ -29,24 +26,13 @@ constexpr int VT = 256;
 __device__ __forceinline__ bool is_cons(const uint32_t* mask, int64_t node) {
   return mask && ((mask[node >> 5] >> (node & 31)) & 1u);
 }
-
-// Fixed-order sum of n partials by one block; result broadcast to all threads.
-__device__ double block_reduce_all(const double* part, int n, double* scratch) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += VT) s += part[i];
-  s = block_sum<VT>(s, scratch);
-  if (threadIdx.x == 0) scratch[0] = s;
-  __syncthreads();
-  const double r = scratch[0];
-  __syncthreads();
-  return r;
-}
 }  // namespace
 
 __global__ void __launch_bounds__(VT)
-    pcg_init_kernel(int64_t n_L, int m, const double* __restrict__ b, const double* __restrict__ d,
-                    double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
-                    double* __restrict__ Ap, const uint32_t* cons_mask, double* part) {
+    pcg_init_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ b,
+                    const double* __restrict__ d, double* __restrict__ x, double* __restrict__ r,
+                    double* __restrict__ p, double* __restrict__ Ap, const uint32_t* cons_mask,
+                    double* part, double* hist) {
   __shared__ double scratch[VT / 32];
   double rr = 0.0, rz = 0.0, cc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * VT;
@@ -68,26 +54,24 @@ __global__ void __launch_bounds__(VT)
   const double s0 = block_sum<VT>(rr, scratch);
   const double s1 = block_sum<VT>(rz, scratch);
   const double s2 = block_sum<VT>(cc, scratch);
+  const int g = gridDim.x;
   if (threadIdx.x == 0) {
     part[blockIdx.x] = s0;
-    part[gridDim.x + blockIdx.x] = s1;
-    part[2 * gridDim.x + blockIdx.x] = s2;
+    part[g + blockIdx.x] = s1;
+    part[2 * g + blockIdx.x] = s2;
   }
-}
-
-__global__ void __launch_bounds__(VT)
-    pcg_init_finalize(PcgState* st, const double* part, int g, double* hist, double* cons_part) {
-  __shared__ double scratch[VT / 32];
-  const double rr = block_reduce_all(part, g, scratch);
-  const double rz = block_reduce_all(part + g, g, scratch);
-  const double cc = block_reduce_all(part + 2 * g, g, scratch);
+  if (!pcg_last_cta(&st->counter[3])) return;
+  const double tr = pcg_sum_partials<VT>(part, g, scratch);
+  const double tz = pcg_sum_partials<VT>(part + g, g, scratch);
+  const double tc = pcg_sum_partials<VT>(part + 2 * g, g, scratch);
   if (threadIdx.x == 0) {
-    cons_part[0] = cc;  // read by the first update kernel as a 1-entry partial list
-    const double norm_b = sqrt(rr);
+    st->counter[3] = 0;
+    const double norm_b = sqrt(tr);  // pcg.cpp:53-64
     st->it = 0;
     st->converged = 0;
     st->error = 0;
     st->stop = 0;
+    st->cons_pp = tc;
     if (!isfinite(norm_b)) {
       st->error = PCG_ERR_RHS;
       st->stop = 1;
@@ -102,39 +86,21 @@ __global__ void __launch_bounds__(VT)
       st->stop = 1;
       return;
     }
-    st->rho[1] = rz;  // rho before iteration 1
+    st->rho = tz;
   }
 }
 
-// Iteration `it` (1-based): alpha prologue + x/r update + r.r, r.z partials.
-// VEC: all vectors 16-byte aligned -> two entries per 128-bit access, two
-// pairs per loop trip (more bytes in flight per thread).
+// Iteration `it` (1-based): x += alpha p, r -= alpha Ap; r.r, r.z partials;
+// the last CTA decides convergence and beta.  VEC: 16-byte aligned vectors,
+// two entries per 128-bit access, two pairs per loop trip.
 template <bool VEC>
 __global__ void __launch_bounds__(VT)
-    pcg_update_kernel(PcgState* st, int it, const double* kpart, int gk, const double* cpart,
-                      int gc, int64_t n, const double* __restrict__ d, double* __restrict__ x,
-                      double* __restrict__ r, const double* __restrict__ p,
-                      const double* __restrict__ Ap, double* part) {
+    pcg_update_kernel(PcgState* st, int it, int64_t n, const double* __restrict__ d,
+                      double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                      const double* __restrict__ Ap, double* part, double* hist) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double pap = block_reduce_all(kpart, gk, scratch) + block_reduce_all(cpart, gc, scratch);
-  const double rho = st->rho[it & 1];
-  // pcg.cpp:74-82
-  if (!isfinite(pap) || pap <= 0.0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->pap = pap;
-      if (!isfinite(pap)) st->error = PCG_ERR_APPLY_NAN;
-      else if (rho == 0.0) st->converged = 1;
-      else st->error = PCG_ERR_INDEFINITE;
-      st->stop = 1;
-    }
-    return;
-  }
-  const double alpha = rho / pap;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->pap = pap;
-    st->alpha = alpha;
-  }
+  const double alpha = st->alpha;
   double rr = 0.0, rz = 0.0;
   const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
@@ -178,47 +144,47 @@ __global__ void __launch_bounds__(VT)
   }
   const double s0 = block_sum<VT>(rr, scratch);
   const double s1 = block_sum<VT>(rz, scratch);
+  const int g = gridDim.x;
   if (threadIdx.x == 0) {
     part[blockIdx.x] = s0;
-    part[gridDim.x + blockIdx.x] = s1;
+    part[g + blockIdx.x] = s1;
+  }
+  if (!pcg_last_cta(&st->counter[1])) return;
+  const double trr = pcg_sum_partials<VT>(part, g, scratch);
+  const double trz = pcg_sum_partials<VT>(part + g, g, scratch);
+  if (threadIdx.x == 0) {
+    st->counter[1] = 0;
+    // pcg.cpp:90-107
+    const double res = sqrt(trr);
+    if (!isfinite(res)) {
+      st->error = PCG_ERR_RESID;
+      st->stop = 1;
+      return;
+    }
+    st->it = it;
+    st->res = res;
+    hist[it] = res;
+    const bool conv = res <= st->target;
+    if (conv) st->converged = 1;
+    if ((conv && !st->fixed) || it == st->limit || res == 0.0) {
+      st->stop = 1;
+      return;
+    }
+    st->beta = trz / st->rho;
+    st->rho = trz;
   }
 }
 
-// Iteration `it`: residual / convergence prologue + p = z + beta p, Ap preset.
+// p = z + beta p, Ap preset; last CTA sums p^2 over constrained rows.
 // VEC: 16-byte aligned vectors and an even component stride n_L.
 template <bool VEC>
 __global__ void __launch_bounds__(VT)
-    pcg_direction_kernel(PcgState* st, int it, const double* upart, int gu, double* hist,
-                         int64_t n_L, int m, const double* __restrict__ d,
+    pcg_direction_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ d,
                          const double* __restrict__ r, double* __restrict__ p,
-                         double* __restrict__ Ap, const uint32_t* cons_mask, double* cpart) {
+                         double* __restrict__ Ap, const uint32_t* cons_mask, double* part) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double rr = block_reduce_all(upart, gu, scratch);
-  const double rz = block_reduce_all(upart + gu, gu, scratch);
-  const double res = sqrt(rr);
-  const double rho = st->rho[it & 1];
-  // pcg.cpp:90-107
-  const bool bad = !isfinite(res);
-  const bool conv = res <= st->target;
-  const bool stop = bad || (conv && !st->fixed) || it == st->limit || res == 0.0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (bad) {
-      st->error = PCG_ERR_RESID;
-    } else {
-      st->it = it;
-      st->res = res;
-      hist[it] = res;
-      if (conv) st->converged = 1;
-    }
-    if (!stop) {
-      st->beta = rz / rho;
-      st->rho[(it + 1) & 1] = rz;
-    }
-    st->stop = stop ? 1 : 0;
-  }
-  if (stop) return;
-  const double beta = rz / rho;
+  const double beta = st->beta;
   double cc = 0.0;
   const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
@@ -230,9 +196,7 @@ __global__ void __launch_bounds__(VT)
       const double2* d2 = reinterpret_cast<const double2*>(d + o);
       double2* p2 = reinterpret_cast<double2*>(p + o);
       double2* a2 = reinterpret_cast<double2*>(Ap + o);
-      for (int64_t k = tid; k < h; k += stride) {
-        const double2 rv = r2[k], pv = p2[k];
-        const double2 dv = d ? d2[k] : make_double2(1.0, 1.0);
+      auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv) {
         double2 q;
         q.x = (d ? rv.x / dv.x : rv.x) + beta * pv.x;
         q.y = (d ? rv.y / dv.y : rv.y) + beta * pv.y;
@@ -242,7 +206,17 @@ __global__ void __launch_bounds__(VT)
         a2[k] = make_double2((w & 1u) ? q.x : 0.0, (w & 2u) ? q.y : 0.0);
         if (w & 1u) cc += q.x * q.x;
         if (w & 2u) cc += q.y * q.y;
+      };
+      const double2 one2 = make_double2(1.0, 1.0);
+      int64_t k = tid;
+      for (; k + stride < h; k += 2 * stride) {
+        const int64_t k1 = k + stride;
+        const double2 ra = r2[k], pa = p2[k], da = d ? d2[k] : one2;
+        const double2 rb = r2[k1], pb = p2[k1], db = d ? d2[k1] : one2;
+        two(k, ra, pa, da);
+        two(k1, rb, pb, db);
       }
+      if (k < h) two(k, r2[k], p2[k], d ? d2[k] : one2);
     } else {
       for (int64_t node = tid; node < n_L; node += stride) {
         const int64_t i = o + node;
@@ -256,7 +230,13 @@ __global__ void __launch_bounds__(VT)
     }
   }
   const double s = block_sum<VT>(cc, scratch);
-  if (threadIdx.x == 0) cpart[blockIdx.x] = s;
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (!pcg_last_cta(&st->counter[2])) return;
+  const double tc = pcg_sum_partials<VT>(part, gridDim.x, scratch);
+  if (threadIdx.x == 0) {
+    st->counter[2] = 0;
+    st->cons_pp = tc;
+  }
 }
 
 // y = x on constrained rows, 0 elsewhere: the RED target of an operator apply
@@ -287,39 +267,32 @@ cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, d
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_init(cudaStream_t s, int64_t n_L, int m, const double* b, const double* d,
-                            double* x, double* r, double* p, double* Ap, const uint32_t* mask,
-                            double* part, PcgState* st, double* hist, double* cons_part) {
-  const int g = vec_grid();
-  pcg_init_kernel<<<g, VT, 0, s>>>(n_L, m, b, d, x, r, p, Ap, mask, part);
-  pcg_init_finalize<<<1, VT, 0, s>>>(st, part, g, hist, cons_part);
-  count_launch(2);
-  return cudaGetLastError();
-}
-
-cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, const double* kpart, int gk,
-                              const double* cpart, int gc, int64_t n, const double* d, double* x,
-                              double* r, const double* p, const double* Ap, double* upart) {
-  if (aligned16(d) && aligned16(x) && aligned16(r) && aligned16(p) && aligned16(Ap))
-    pcg_update_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r, p,
-                                                     Ap, upart);
-  else
-    pcg_update_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, kpart, gk, cpart, gc, n, d, x, r,
-                                                      p, Ap, upart);
+cudaError_t pcg_launch_init(cudaStream_t s, PcgState* st, int64_t n_L, int m, const double* b,
+                            const double* d, double* x, double* r, double* p, double* Ap,
+                            const uint32_t* mask, double* part, double* hist) {
+  pcg_init_kernel<<<vec_grid(), VT, 0, s>>>(st, n_L, m, b, d, x, r, p, Ap, mask, part, hist);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, const double* upart,
-                                 double* hist, int64_t n_L, int m, const double* d,
-                                 const double* r, double* p, double* Ap, const uint32_t* mask,
-                                 double* cpart) {
-  if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
-    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m,
-                                                        d, r, p, Ap, mask, cpart);
+cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n, const double* d,
+                              double* x, double* r, const double* p, const double* Ap,
+                              double* part, double* hist) {
+  if (aligned16(d) && aligned16(x) && aligned16(r) && aligned16(p) && aligned16(Ap))
+    pcg_update_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, n, d, x, r, p, Ap, part, hist);
   else
-    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, upart, vec_grid(), hist, n_L, m,
-                                                         d, r, p, Ap, mask, cpart);
+    pcg_update_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, n, d, x, r, p, Ap, part, hist);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int64_t n_L, int m,
+                                 const double* d, const double* r, double* p, double* Ap,
+                                 const uint32_t* mask, double* part) {
+  if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
+    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, n_L, m, d, r, p, Ap, mask, part);
+  else
+    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, n_L, m, d, r, p, Ap, mask, part);
   count_launch();
   return cudaGetLastError();
 }
