@@ -186,7 +186,7 @@ struct hxf_op {
   double* d_part = nullptr;
   double *d_B = nullptr, *d_G = nullptr, *d_Bt = nullptr, *d_Gt = nullptr;
   double *d_bb = nullptr, *d_dd = nullptr, *d_bd = nullptr;
-  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_vpart, w_hist, w_ediag, w_ldiag;
+  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_dinv, w_vpart, w_hist, w_ediag, w_ldiag;
   PcgState* d_state = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
@@ -213,7 +213,7 @@ struct hxf_op {
                       (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
                       (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state})
       if (ptr) cudaFree(ptr);
-    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_vpart, &w_hist, &w_ediag,
+    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
                       &w_ldiag})
       v->release();
     for (auto e : ev) cudaEventDestroy(e);
@@ -815,6 +815,7 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     double* r = op->w_r.ensure(n);
     double* p = op->w_p.ensure(n);
     double* Ap = op->w_Ap.ensure(n);
+    double* dinv = dd ? op->w_dinv.ensure(n) : nullptr;  // 1/diag, filled by the init kernel
     const int vg = vec_grid();
     double* vpart = op->w_vpart.ensure(size_t(3 * vg));  // per-CTA partials (<= 3 per CTA)
     double* hist = op->w_hist.ensure(size_t(limit) + 2);
@@ -839,14 +840,14 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
       // Ap was preset by the init / direction kernel: no memset pass here
       device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state);
       record(op->ev[2 * (it - 1) + 1]);
-      ck(pcg_launch_update(s, op->d_state, it, int64_t(n), dd, dx, r, p, Ap, vpart, hist),
+      ck(pcg_launch_update(s, op->d_state, it, int64_t(n), dinv, dx, r, p, Ap, vpart, hist),
          "pcg update");
-      ck(pcg_launch_direction(s, op->d_state, op->n_L, op->m, dd, r, p, Ap, op->d_mask, vpart),
+      ck(pcg_launch_direction(s, op->d_state, op->n_L, op->m, dinv, r, p, Ap, op->d_mask, vpart),
          "pcg direction");
     };
     auto init = [&] {
-      ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, db, dd, dx, r, p, Ap, op->d_mask, vpart,
-                         hist),
+      ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, db, dd, dinv, dx, r, p, Ap, op->d_mask,
+                         vpart, hist),
          "pcg init");
     };
 
@@ -856,7 +857,7 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     if (fixed) {
       // benchmark semantics: the whole fixed-iteration solve as one CUDA graph
       // (launch-gap free), captured once per operand set and replayed
-      const std::vector<const void*> key = {db, dd, dx, (const void*)(intptr_t)limit};
+      const std::vector<const void*> key = {db, dd, dx, dinv, (const void*)(intptr_t)limit};
       if (!op->graph_exec || op->graph_key != key) {
         if (op->graph_exec) cudaGraphExecDestroy(op->graph_exec);
         op->graph_exec = nullptr;

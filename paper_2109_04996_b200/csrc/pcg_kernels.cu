@@ -30,7 +30,8 @@ __device__ __forceinline__ bool is_cons(const uint32_t* mask, int64_t node) {
 
 __global__ void __launch_bounds__(VT)
     pcg_init_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ b,
-                    const double* __restrict__ d, double* __restrict__ x, double* __restrict__ r,
+                    const double* __restrict__ d, double* __restrict__ dinv,
+                    double* __restrict__ x, double* __restrict__ r,
                     double* __restrict__ p, double* __restrict__ Ap, const uint32_t* cons_mask,
                     double* part, double* hist) {
   __shared__ double scratch[VT / 32];
@@ -40,7 +41,12 @@ __global__ void __launch_bounds__(VT)
     for (int64_t node = (int64_t)blockIdx.x * VT + threadIdx.x; node < n_L; node += stride) {
       const int64_t i = c * n_L + node;
       const double bi = b[i];
-      const double zi = d ? bi / d[i] : bi;
+      double zi = bi;
+      if (d) {
+        const double di = 1.0 / d[i];  // Jacobi z = r / d as z = r * (1/d), once per solve
+        dinv[i] = di;
+        zi = bi * di;
+      }
       const bool cons = is_cons(cons_mask, node);
       x[i] = 0.0;
       r[i] = bi;
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(VT)
 // the last CTA decides convergence and beta.  VEC: 16-byte aligned vectors,
 // two entries per 128-bit access, two pairs per loop trip.
 template <bool VEC>
-__global__ void __launch_bounds__(VT)
+__global__ void __launch_bounds__(VT, 4)
     pcg_update_kernel(PcgState* st, int it, int64_t n, const double* __restrict__ d,
                       double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                       const double* __restrict__ Ap, double* part, double* hist) {
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(VT)
     const double ri = r[i] - alpha * Ap[i];
     r[i] = ri;
     rr += ri * ri;
-    rz += ri * (d ? ri / d[i] : ri);
+    rz += ri * (d ? ri * d[i] : ri);  // d holds 1/diag here
   };
   if constexpr (VEC) {
     const int64_t n2 = n / 2;
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(VT)
       reinterpret_cast<double2*>(x)[k] = xv;
       reinterpret_cast<double2*>(r)[k] = rv;
       rr += rv.x * rv.x + rv.y * rv.y;
-      rz += rv.x * (d ? rv.x / dv.x : rv.x) + rv.y * (d ? rv.y / dv.y : rv.y);
+      rz += rv.x * (rv.x * dv.x) + rv.y * (rv.y * dv.y);  // dv = 1/diag (or 1)
     };
     const double2* x2 = reinterpret_cast<const double2*>(x);
     const double2* p2 = reinterpret_cast<const double2*>(p);
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(VT)
 // p = z + beta p, Ap preset; last CTA sums p^2 over constrained rows.
 // VEC: 16-byte aligned vectors and an even component stride n_L.
 template <bool VEC>
-__global__ void __launch_bounds__(VT)
+__global__ void __launch_bounds__(VT, 4)
     pcg_direction_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ d,
                          const double* __restrict__ r, double* __restrict__ p,
                          double* __restrict__ Ap, const uint32_t* cons_mask, double* part) {
@@ -198,8 +204,8 @@ __global__ void __launch_bounds__(VT)
       double2* a2 = reinterpret_cast<double2*>(Ap + o);
       auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv) {
         double2 q;
-        q.x = (d ? rv.x / dv.x : rv.x) + beta * pv.x;
-        q.y = (d ? rv.y / dv.y : rv.y) + beta * pv.y;
+        q.x = rv.x * dv.x + beta * pv.x;  // dv = 1/diag (or 1)
+        q.y = rv.y * dv.y + beta * pv.y;
         p2[k] = q;
         const int64_t node = 2 * k;
         const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(VT)
     } else {
       for (int64_t node = tid; node < n_L; node += stride) {
         const int64_t i = o + node;
-        const double zi = d ? r[i] / d[i] : r[i];
+        const double zi = d ? r[i] * d[i] : r[i];  // d holds 1/diag here
         const double pi = zi + beta * p[i];
         const bool cons = is_cons(cons_mask, node);
         p[i] = pi;
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(VT)
 }
 
 // ------------------------------------------------------------------ host side
-int vec_grid() { return num_sms() * 8; }
+int vec_grid() { return num_sms() * 4; }
 
 namespace {
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -268,9 +274,9 @@ cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, d
 }
 
 cudaError_t pcg_launch_init(cudaStream_t s, PcgState* st, int64_t n_L, int m, const double* b,
-                            const double* d, double* x, double* r, double* p, double* Ap,
-                            const uint32_t* mask, double* part, double* hist) {
-  pcg_init_kernel<<<vec_grid(), VT, 0, s>>>(st, n_L, m, b, d, x, r, p, Ap, mask, part, hist);
+                            const double* d, double* dinv, double* x, double* r, double* p,
+                            double* Ap, const uint32_t* mask, double* part, double* hist) {
+  pcg_init_kernel<<<vec_grid(), VT, 0, s>>>(st, n_L, m, b, d, dinv, x, r, p, Ap, mask, part, hist);
   count_launch();
   return cudaGetLastError();
 }
