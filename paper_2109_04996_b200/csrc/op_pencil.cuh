@@ -44,12 +44,17 @@ struct PencilTraits {
   static constexpr int NT = pencil_round_up(EPB * PP, 32);
   static constexpr bool SWZ = (P == 8);  // XOR-rotated 64-byte rows
   static constexpr int RS = SWZ ? 8 : pencil_row_stride(P);
-  static constexpr int PL = P * RS + 8;  // plane stride: +64 B skews consecutive planes by 16 banks
+  // plane stride: padded layouts skew consecutive planes by 16 banks (+64 B);
+  // the swizzled p = 7 layout flips the row parity per plane instead (no pad)
+  static constexpr int PL = SWZ ? P * RS : P * RS + 8;
   static constexpr int SLAB = P * PL;    // doubles per element slab
   static constexpr int QDS = 6 * P3;     // geometric factors per element (even)
   static constexpr int DR = pencil_round_up(P, 2);  // matrix row stride (16-byte rows)
+  // D^T rows in shared memory too, except for p = 7 where the 512 B are what
+  // it takes to fit 6 CTAs per SM (transposed rows read as D columns there)
+  static constexpr bool DT_SMEM = !SWZ;
   static constexpr int OFF_D = 0;                   // [P][DR] D, then [P][DR] D^T
-  static constexpr int OFF_QD = 2 * P * DR;
+  static constexpr int OFF_QD = (DT_SMEM ? 2 : 1) * P * DR;
   static constexpr int OFF_A = OFF_QD + EPB * QDS;
   static constexpr int OFF_B = OFF_A + EPB * SLAB;
   static constexpr int OFF_C = OFF_B + EPB * SLAB;
@@ -57,12 +62,18 @@ struct PencilTraits {
 
   // slab offset of point (i, j, k) — x index i, y index j, plane k
   __device__ static __forceinline__ int off(int k, int j, int i) {
-    if constexpr (SWZ) return k * PL + j * RS + 2 * (((i >> 1) + (j >> 1)) & 3) + (i & 1);
+    if constexpr (SWZ) {
+      const int R = j ^ (k & 1);  // physical row: parity flips plane to plane
+      return k * PL + R * RS + 2 * (((i >> 1) + (R >> 1)) & 3) + (i & 1);
+    }
     return k * PL + j * RS + i;
   }
   // slab offset of the 16-byte chunk holding x indices (2c, 2c+1) of row (j, k)
   __device__ static __forceinline__ int chunk(int k, int j, int c) {
-    if constexpr (SWZ) return k * PL + j * RS + 2 * ((c + (j >> 1)) & 3);
+    if constexpr (SWZ) {
+      const int R = j ^ (k & 1);
+      return k * PL + R * RS + 2 * ((c + (R >> 1)) & 3);
+    }
     return k * PL + j * RS + 2 * c;
   }
 };
@@ -103,6 +114,15 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   const int la = l % P, lb = l / P;  // (i,j) | (j,k) | (i,k) depending on the phase
   const double* sD = smem + T::OFF_D;
   const double* sDT = smem + T::OFF_D + P * DR;
+  // row o of D^T (= column o of D)
+  auto load_trow = [&](int o, double* d) {
+    if constexpr (T::DT_SMEM) {
+      load_row<P>(sDT + o * DR, d);
+    } else {
+#pragma unroll
+      for (int a = 0; a < P; ++a) d[a] = sD[a * DR + o];
+    }
+  };
   double* sQD = smem + T::OFF_QD;
   double* SA = smem + T::OFF_A + (active_slot ? slot : 0) * T::SLAB;
   double* SB = smem + T::OFF_B + (active_slot ? slot : 0) * T::SLAB;
@@ -111,8 +131,8 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
 
   for (int t = tid; t < P * P; t += NT) {
     const int r = t / P, c = t % P;
-    smem[T::OFF_D + r * DR + c] = prm.D[t];           // D[r][c]
-    smem[T::OFF_D + P * DR + c * DR + r] = prm.D[t];  // D^T[c][r]
+    smem[T::OFF_D + r * DR + c] = prm.D[t];                            // D[r][c]
+    if (T::DT_SMEM) smem[T::OFF_D + P * DR + c * DR + r] = prm.D[t];  // D^T[c][r]
   }
 
   const int64_t nsteps = (prm.E + EPB - 1) / EPB;
@@ -301,7 +321,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
 #pragma unroll
         for (int o = 0; o < P; ++o) {
           double d[P];
-          load_row<P>(sDT + o * DR, d);
+          load_trow(o, d);
           double sx = 0.0, sy = 0.0;
 #pragma unroll
           for (int a = 0; a < P; ++a) {
@@ -323,7 +343,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           double d[P];
-          load_row<P>(sDT + k * DR, d);
+          load_trow(k, d);
           double s = 0.0;
 #pragma unroll
           for (int cc = 0; cc < P; ++cc) s += d[cc] * v2[cc];
