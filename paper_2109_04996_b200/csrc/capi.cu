@@ -129,13 +129,17 @@ int ablate_bits() {
   return bits;
 }
 
-bool pencil_disabled() {
-  static const bool off = [] {
+int op_kernel_choice() {
+  static const int choice = [] {
     const char* v = std::getenv("HXF_OP_KERNEL");
-    return v && std::string(v) == "generic";
+    if (!v) return 0;
+    const std::string s(v);
+    return s == "pencil" ? 1 : (s == "generic" ? 2 : 0);
   }();
-  return off;
+  return choice;
 }
+
+bool pencil_disabled() { return op_kernel_choice() == 2; }
 
 int max_op_grid() { return num_sms() * 32; }
 

@@ -79,7 +79,10 @@ HXF_DECL_P(16)
 #undef HXF_DECL_P
 
 int num_sms();
-// HXF_OP_KERNEL=generic forces the generic fused kernel (A/B comparisons).
+// HXF_OP_KERNEL selects the collocated fast path for A/B comparisons:
+// unset/"dmma" -> 0 (tensor-core kernel where available), "pencil" -> 1,
+// "generic" -> 2 (op_kernel.cuh only).
+int op_kernel_choice();
 bool pencil_disabled();
 int ablate_bits();
 void count_launch(int n = 1);

@@ -1,0 +1,309 @@
+// K1 (collocated BP5/BP6, p = 7): fused operator on the FP64 tensor cores.
+//   y = G^T D^T S D G x,  every 1-D contraction an 8x8x8 matrix product.
+//
+// The pencil kernel (op_pencil.cuh) is issue-bound: with all memory traffic
+// ablated it still takes ~90 us at C3 (2400 warp-instructions per element).
+// Here each 1-D contraction of an 8x8 slice is two DMMA m8n8k4 (FP64 tensor
+// core, mma.sync) instructions instead of 64 DFMA lanes-worth, cutting the
+// instruction count per element ~4x; the arithmetic (and its FP64 rounding
+// model: fused multiply-adds) is unchanged.
+//
+// One element per CTA of two warps; lane l: g = l>>2, t = l&3 (the mma
+// fragment coordinates).  "dist X": a lane owns points (k, j = g, i = 2t..2t+1)
+// of the warp's planes k in {4w..4w+3}; "dist Z": (k = g, j, i = 2t..2t+1) for
+// the warp's rows j in {4w..4w+3}.
+//   x-dir  G0_k = U_k D^T    (M = j, N = o, K = a)  -> dist X, registers
+//   y-dir  G1_k = D U_k      (M = o, N = i, K = b)  -> dist X, registers
+//   z-dir  G2_j = D U_(.j.)  (M = o, N = i, K = c)  -> dist Z -> slab Z
+//   QFunction on dist X (factors from the TMA-staged slab), V0 -> A, V1 -> B,
+//   V2 -> Z;  x^T and y^T accumulate into one fragment (dist X), z^T lands in
+//   dist Z and is transposed through slab B before the FP64 RED scatter.
+// The only D operands a lane ever needs are D[g][4ks+t] and D[4ks+t][g]
+// (4 registers).  Slabs are [k][R][col] with R = j ^ (k & 1) and the 16-byte
+// half of each row flipped by bit 1 of R, which keeps every fragment load at
+// its 2-wavefront minimum and every dist-X / dist-Z pair access at 4.
+// Gather software-pipelined (next item's z-lines in registers), geometric
+// factors by one bulk async copy (TMA engine, L2 evict_first) per element,
+// issued as soon as the previous element's QFunction consumed them.
+// Reference semantics: proj/src/operator.cpp:64-144 (see op_kernel.cuh).
+#pragma once
+#include "hxf_device.cuh"
+#include "hxf_internal.h"
+#include "pcg_device.cuh"
+
+namespace hxf {
+
+template <int NC_, int GM_>
+struct DmmaTraits {
+  static constexpr int P = 8, NC = NC_, GM = GM_, P3 = 512, NT = 64;
+  static constexpr int SLAB = 512;   // doubles
+  static constexpr int QDS = 6 * P3;
+  static constexpr int OFF_QD = 0;
+  static constexpr int OFF_A = QDS;  // U, then V0
+  static constexpr int OFF_B = OFF_A + SLAB;  // V1, then Y2 (dist-Z -> dist-X transpose)
+  static constexpr int OFF_Z = OFF_B + SLAB;  // G2, then V2
+  static constexpr int SMEM_BYTES = (OFF_Z + SLAB) * 8;
+
+  __device__ static __forceinline__ int off(int k, int j, int i) {
+    const int R = j ^ (k & 1);
+    return k * 64 + R * 8 + (i ^ (((R >> 1) & 1) << 2));
+  }
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <class T>
+__global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
+  constexpr int NC = T::NC, P3 = T::P3, NT = T::NT;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t qbar;
+  __shared__ double red_scratch[NT / 32 + 1];
+  if (prm.stop && *prm.stop) return;
+
+  const int tid = threadIdx.x;
+  const int w = tid >> 5, l = tid & 31, g = l >> 2, t = l & 3;
+  double* sQD = smem + T::OFF_QD;
+  double* SA = smem + T::OFF_A;
+  double* SB = smem + T::OFF_B;
+  double* SZ = smem + T::OFF_Z;
+
+  // the only D entries this lane ever multiplies by (fragment coordinates)
+  double Dr[2], Dc[2];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    Dr[ks] = __ldg(prm.D + g * 8 + ks * 4 + t);    // D[g][4ks+t]
+    Dc[ks] = __ldg(prm.D + (ks * 4 + t) * 8 + g);  // D[4ks+t][g]
+  }
+
+  const int64_t nsteps = prm.E;
+  const int64_t G = gridDim.x;
+  const int64_t NXY = prm.NX * prm.NY;
+  uint64_t policy = 0;
+  auto issue_qdata = [&](int64_t e) {
+    mbar_arrive_expect_tx(&qbar, (uint32_t)(T::QDS * 8));
+    bulk_g2s(sQD, prm.qd + e * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);
+  };
+  if (tid == 0) {
+    mbar_init(&qbar, 1);
+    fence_mbar_init();
+    policy = l2_evict_first_policy();
+    if ((int64_t)blockIdx.x < nsteps && !(prm.ablate & 4)) issue_qdata(blockIdx.x);
+  }
+
+  // Gather geometry of one element for this lane: node of (i = 2t, j = g,
+  // k = 4w) and constraint bits (bit 2*kk + h: node (i = 2t + h, k = 4w + kk)).
+  struct Geo {
+    int64_t key;
+    uint32_t cmask;
+    bool active;
+  };
+  auto node_of = [&](const Geo& q, int kk, int h) -> int64_t {
+    if constexpr (T::GM == 0) return q.key + (int64_t)kk * NXY + h;
+    if (prm.idx)
+      return (int64_t)prm.idx[q.key * P3 + (2 * t + h) + 8 * (g + 8 * (4 * w + kk))];
+    return q.key + (int64_t)kk * NXY + h;
+  };
+  auto geometry = [&](int64_t e) {
+    Geo q{};
+    q.active = e < nsteps;
+    if (!q.active) return q;
+    if (T::GM == 1 && prm.idx) {
+      q.key = e;
+    } else {
+      const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
+      const int64_t ix = ex * 7 + 2 * t, iy = ey * 7 + g, iz = ez * 7 + 4 * w;
+      q.key = ix + prm.NX * iy + NXY * iz;
+      if (T::GM == 0 && prm.cons_mode == 1) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t x = ix + h, z = iz + kk;
+            if (x == 0 || x == prm.NX - 1 || iy == 0 || iy == prm.NY - 1 || z == 0 ||
+                z == prm.NZ - 1)
+              q.cmask |= 1u << (2 * kk + h);
+          }
+      }
+    }
+    if (T::GM == 1 && prm.cons_mode == 2) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t node = node_of(q, kk, h);
+          q.cmask |= ((prm.cons_mask[node >> 5] >> (node & 31)) & 1u) << (2 * kk + h);
+        }
+    }
+    return q;
+  };
+  auto load_lines = [&](const Geo& q, int c, double* xn) {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        xn[2 * kk + h] = (q.active && !(prm.ablate & 1))
+                             ? __ldg(prm.x + c * prm.n_L + node_of(q, kk, h))
+                             : 1.0;
+  };
+
+  Geo gcur = geometry(blockIdx.x);
+  Geo gpf = NC > 1 ? gcur : geometry(blockIdx.x + G);
+  double xn[8];
+  load_lines(gcur, 0, xn);
+  double u[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
+  load_lines(gpf, 1 % NC, xn);
+  __syncthreads();  // mbarrier init visible
+
+  double dot_acc = 0.0;
+  int it = 0, q = 0;
+#pragma unroll 1
+  for (int64_t e = blockIdx.x; e < nsteps; e += G, ++it) {
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c, ++q) {
+      double* yc = prm.y + c * prm.n_L;
+      // ---- G: this lane's masked dist-X pairs into slab A ----
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        *reinterpret_cast<double2*>(SA + T::off(4 * w + kk, g, 2 * t)) =
+            make_double2(u[2 * kk], u[2 * kk + 1]);
+      // next item's raw lines: land while this item computes
+      {
+        const Geo gnext = ((q + 2) / NC == (q + 1) / NC && NC > 1)
+                              ? gpf
+                              : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
+        double nx_[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) nx_[m] = xn[m];
+        // masked values of item q+1 are formed when it starts (gpf)
+        load_lines(gnext, (q + 2) % NC, xn);
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          u[m] = (gpf.active && !((gpf.cmask >> m) & 1u)) ? nx_[m] : 0.0;  // item q+1
+        gpf = gnext;
+      }
+      __syncthreads();  // (A) slab A complete
+
+      // ---- forward contractions ----
+      double g0[4][2], g1[4][2];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * w + kk;
+        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          dmma(c0, c1, SA[T::off(k, g, 4 * ks + t)], Dr[ks]);  // x: U_k[j][a] . D^T[a][o]
+          dmma(d0, d1, Dr[ks], SA[T::off(k, 4 * ks + t, g)]);  // y: D[o][b] . U_k[b][i]
+        }
+        g0[kk][0] = c0;
+        g0[kk][1] = c1;
+        g1[kk][0] = d0;
+        g1[kk][1] = d1;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * w + jj;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dr[ks], SA[T::off(4 * ks + t, j, g)]);
+        *reinterpret_cast<double2*>(SZ + T::off(g, j, 2 * t)) = make_double2(c0, c1);  // dist Z
+      }
+      if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
+      __syncthreads();  // (B) G2 complete, slab A free
+
+      // ---- QFunction on dist X (qfunction.cpp:135-162) ----
+      double energy = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * w + kk;
+        const int sp = T::off(k, g, 2 * t);
+        const double2 z2 = *reinterpret_cast<const double2*>(SZ + sp);
+        const int pt = k * 64 + g * 8 + 2 * t;
+        double2 s[6];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) s[m] = *reinterpret_cast<const double2*>(sQD + m * P3 + pt);
+        double v0[2], v1[2], v2[2];
+        const double gz[2] = {z2.x, z2.y};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double a0 = g0[kk][h], a1 = g1[kk][h], a2 = gz[h];
+          const double s00 = h ? s[0].y : s[0].x, s01 = h ? s[1].y : s[1].x;
+          const double s02 = h ? s[2].y : s[2].x, s11 = h ? s[3].y : s[3].x;
+          const double s12 = h ? s[4].y : s[4].x, s22 = h ? s[5].y : s[5].x;
+          v0[h] = s00 * a0 + s01 * a1 + s02 * a2;
+          v1[h] = s01 * a0 + s11 * a1 + s12 * a2;
+          v2[h] = s02 * a0 + s12 * a1 + s22 * a2;
+          // p.(A p) over free nodes = sum_points grad u . S grad u
+          energy += a0 * v0[h] + a1 * v1[h] + a2 * v2[h];
+        }
+        *reinterpret_cast<double2*>(SA + sp) = make_double2(v0[0], v0[1]);
+        *reinterpret_cast<double2*>(SB + sp) = make_double2(v1[0], v1[1]);
+        *reinterpret_cast<double2*>(SZ + sp) = make_double2(v2[0], v2[1]);
+      }
+      dot_acc += prm.coef * energy;
+      if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
+      __syncthreads();  // (C) V0, V1, V2 complete
+      if (c == NC - 1 && tid == 0 && e + G < nsteps && !(prm.ablate & 4)) issue_qdata(e + G);
+
+      // ---- transposed contractions ----
+      double y01[4][2];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * w + kk;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          dmma(c0, c1, SA[T::off(k, g, 4 * ks + t)], Dc[ks]);  // x^T: V0_k[j][a] . D[a][i]
+          dmma(c0, c1, Dc[ks], SB[T::off(k, 4 * ks + t, g)]);  // y^T: D^T[j][b] . V1_k[b][i]
+        }
+        y01[kk][0] = c0;
+        y01[kk][1] = c1;
+      }
+      double y2z[4][2];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = 4 * w + jj;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dc[ks], SZ[T::off(4 * ks + t, j, g)]);  // z^T
+        y2z[jj][0] = c0;
+        y2z[jj][1] = c1;
+      }
+      __syncthreads();  // (D) slab B (V1) free
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+        *reinterpret_cast<double2*>(SB + T::off(g, 4 * w + jj, 2 * t)) =
+            make_double2(y2z[jj][0], y2z[jj][1]);
+      __syncthreads();  // (E) Y2 in slab B (dist Z)
+
+      // ---- combine on dist X, G^T scatter (constrained rows preset by the caller) ----
+      if (gcur.active) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const double2 z2 = *reinterpret_cast<const double2*>(SB + T::off(4 * w + kk, g, 2 * t));
+          const double yk0 = prm.coef * (y01[kk][0] + z2.x);
+          const double yk1 = prm.coef * (y01[kk][1] + z2.y);
+          if (!(prm.ablate & 2)) {
+            if (!((gcur.cmask >> (2 * kk)) & 1u)) red_add(yc + node_of(gcur, kk, 0), yk0);
+            if (!((gcur.cmask >> (2 * kk + 1)) & 1u)) red_add(yc + node_of(gcur, kk, 1), yk1);
+          }
+        }
+      }
+      __syncthreads();  // (F) slab B free for the next item
+    }
+    gcur = geometry(e + G);
+  }
+
+  if (prm.dot_partials) {
+    const double s = block_sum<NT>(dot_acc, red_scratch);
+    if (tid == 0) prm.dot_partials[blockIdx.x] = s;
+    pcg_alpha_epilogue<NT>(prm.fin, red_scratch);
+  }
+}
+
+}  // namespace hxf

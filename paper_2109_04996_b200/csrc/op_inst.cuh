@@ -4,6 +4,7 @@
 
 #include "op_kernel.cuh"
 #include "op_pencil.cuh"
+#include "op_dmma.cuh"
 
 namespace hxf {
 namespace {
@@ -72,6 +73,36 @@ cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int
   return cudaGetLastError();
 }
 
+// p = 7 collocated diffusion on the FP64 tensor cores (op_dmma.cuh).
+template <class T>
+cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_dmma_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  if (!prm.D) return cudaErrorInvalidValue;
+  const int grid = (int)(prm.E < max_ctas ? prm.E : max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int NC>
+cudaError_t run_dmma_gm(const OpParams& prm, cudaStream_t s, int* g) {
+  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0>>(prm, s, g);
+  return run_dmma<DmmaTraits<NC, 1>>(prm, s, g);
+}
+
 template <int P, int NC>
 constexpr bool use_pencil() {
   return P <= 10 && PencilTraits<P, NC, 0>::SMEM_BYTES <= 112 * 1024;
@@ -86,6 +117,12 @@ cudaError_t run_pencil_gm(const OpParams& prm, const double* D, cudaStream_t s, 
 template <int P, int Q, bool INTERP>
 cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const double* D,
                   cudaStream_t s, int* g) {
+  if constexpr (!INTERP && P == 8) {
+    if (qk == 1 && op_kernel_choice() == 0) {
+      if (NC == 1) return run_dmma_gm<1>(prm, s, g);
+      if (NC == 3) return run_dmma_gm<3>(prm, s, g);
+    }
+  }
   if constexpr (!INTERP) {
     if (qk == 1 && NC == 1 && use_pencil<P, 1>() && !pencil_disabled())
       return run_pencil_gm<P, 1>(prm, D, s, g);
