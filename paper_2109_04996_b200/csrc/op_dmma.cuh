@@ -141,13 +141,25 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
     return q;
   };
   auto load_lines = [&](const Geo& q, int c, double* xn) {
+    const double* xc = prm.x + c * prm.n_L;
+    // structured box: a lane's node pair (i = 2t, 2t+1) is 16-byte aligned iff
+    // its first node is even (uniform across the element when NX, n_L even)
+    if (T::GM == 0 && q.active && !(prm.ablate & 1) && ((reinterpret_cast<uintptr_t>(xc) +
+                                                         8 * q.key) & 15u) == 0 &&
+        (prm.NX & 1) == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xc + node_of(q, kk, 0)));
+        xn[2 * kk] = v.x;
+        xn[2 * kk + 1] = v.y;
+      }
+      return;
+    }
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        xn[2 * kk + h] = (q.active && !(prm.ablate & 1))
-                             ? __ldg(prm.x + c * prm.n_L + node_of(q, kk, h))
-                             : 1.0;
+        xn[2 * kk + h] = (q.active && !(prm.ablate & 1)) ? __ldg(xc + node_of(q, kk, h)) : 1.0;
   };
 
   Geo gcur = geometry(blockIdx.x);
