@@ -152,6 +152,14 @@ def profiled_traffic():
         return None
 
 
+def op_kernel_name():
+    import os as _os
+    choice = _os.environ.get("HXF_OP_KERNEL", "dmma")
+    return {"dmma": "hxf::op_dmma_kernel (FP64 tensor-core fused G^T B^T D B G)",
+            "pencil": "hxf::op_pencil_kernel (fused G^T B^T D B G, DFMA pencils)",
+            "generic": "hxf::op_apply_kernel (generic fused G^T B^T D B G)"}.get(choice, choice)
+
+
 def cpu_baseline(args, sizes):
     """The reference's own run_bench on this host's cores (oracle/_ref)."""
     import oracle
@@ -326,7 +334,7 @@ def run_ours(args):
                     "operator_kernel_us": t_k1 * 1e6},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": profiled_traffic(),
-                     "kernel": "hxf::op_apply_kernel (fused G^T B^T D B G)",
+                     "kernel": op_kernel_name(),
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_vec,
                 "d2h_bytes_per_step": 8 * n_vec},
