@@ -155,6 +155,47 @@ typedef struct {
 int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_options* opts,
             double* x, hxf_memspace space, hxf_solve_report* report);
 
+/* ---- partitioned box (multi-GPU) ---------------------------
+ * The reference has no distributed layer (shared-memory threads only,
+ * proj/src/parallel.cpp); this is the B200 extension its paper describes as
+ * the gather-scatter P operator.  Each rank holds the
+ * structured operator of one sub-box of the element grid; its L-vector is the
+ * sub-box's own node lattice, interface planes duplicated.  A partitioned
+ * operator's apply ends with an interface sum-exchange so every copy of an
+ * interface node holds the assembled value; PCG dots weigh each node once
+ * (owner = the sub-box in which it is not on a low interface plane) and are
+ * all-reduced.  Restriction / basis / qfunction entry points stay local. */
+typedef struct hxf_comm hxf_comm;
+typedef struct hxf_comm_group hxf_comm_group;
+#define HXF_COMM_ID_BYTES 128
+
+/* NCCL (dlopen of libnccl.so.2): one rank per GPU.  Rank 0 makes the id and
+ * distributes it (e.g. over torch.distributed); every rank then creates. */
+int hxf_comm_unique_id(unsigned char id[HXF_COMM_ID_BYTES]);
+int hxf_comm_create_nccl(hxf_ctx* ctx, int nranks, int rank, const unsigned char id[HXF_COMM_ID_BYTES],
+                         hxf_comm** out);
+/* Wrap a caller-owned ncclComm_t (not destroyed by hxf_comm_destroy). */
+int hxf_comm_wrap_nccl(hxf_ctx* ctx, void* nccl_comm, hxf_comm** out);
+/* In-process group: nranks sub-domains driven by nranks host threads (one
+ * context each, any devices).  Host-synchronous, for tests and debugging. */
+int hxf_comm_group_create(int nranks, hxf_comm_group** out);
+int hxf_comm_group_destroy(hxf_comm_group* group);
+int hxf_comm_create_group(hxf_ctx* ctx, hxf_comm_group* group, int rank, hxf_comm** out);
+int hxf_comm_destroy(hxf_comm* comm);
+int hxf_comm_rank(const hxf_comm* comm);
+int hxf_comm_size(const hxf_comm* comm);
+/* In-place sum over ranks of n doubles (device memory), on the stream (NULL = ctx stream). */
+int hxf_comm_allreduce_sum(hxf_comm* comm, double* dev, int64_t n, void* stream);
+
+typedef struct {
+  int neighbor[3][2]; /* rank sharing this lattice's low / high face plane, per axis; -1 = none */
+} hxf_partition_desc;
+/* Attach a structured-box operator to a partition.  The constrained list
+ * given at create time must already be the global-boundary faces only. */
+int hxf_operator_set_partition(hxf_op* op, hxf_comm* comm, const hxf_partition_desc* desc);
+/* Interface sum-exchange of an L-vector in place (the P^T P of the paper). */
+int hxf_operator_halo_sum(hxf_op* op, double* v, hxf_memspace space);
+
 #ifdef __cplusplus
 }
 #endif

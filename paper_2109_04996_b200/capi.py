@@ -26,6 +26,10 @@ EXPORTS = (
     "hxf_operator_diagonal", "hxf_restriction_apply", "hxf_restriction_multiplicity",
     "hxf_basis_apply", "hxf_qfunction_apply", "hxf_qdata_compute", "hxf_pcg",
     "hxf_malloc", "hxf_free", "hxf_memcpy", "hxf_synchronize",
+    "hxf_comm_unique_id", "hxf_comm_create_nccl", "hxf_comm_wrap_nccl", "hxf_comm_group_create",
+    "hxf_comm_group_destroy", "hxf_comm_create_group", "hxf_comm_destroy", "hxf_comm_rank",
+    "hxf_comm_size", "hxf_comm_allreduce_sum", "hxf_operator_set_partition",
+    "hxf_operator_halo_sum",
 )
 
 
@@ -41,6 +45,10 @@ class HxfInvalidArgument(HxfError, ValueError):
 
 class HxfNumericError(HxfError):
     """HXF_ENUMERIC — the reference's std::runtime_error."""
+
+
+class PartitionDesc(C.Structure):
+    _fields_ = [("neighbor", (C.c_int * 2) * 3)]
 
 
 class OperatorDesc(C.Structure):
@@ -98,6 +106,18 @@ def lib() -> C.CDLL:
     L.hxf_qfunction_apply.argtypes = [P, I, P, I64, I, I64, I64, P, P, I]
     L.hxf_qdata_compute.argtypes = [P, I, I, P, P, P, I64, I64, P, P, P, I, P, I]
     L.hxf_pcg.argtypes = [P, P, P, C.POINTER(PcgOptions), P, I, C.POINTER(SolveReport)]
+    L.hxf_comm_unique_id.argtypes = [P]
+    L.hxf_comm_create_nccl.argtypes = [P, I, I, P, C.POINTER(P)]
+    L.hxf_comm_wrap_nccl.argtypes = [P, P, C.POINTER(P)]
+    L.hxf_comm_group_create.argtypes = [I, C.POINTER(P)]
+    L.hxf_comm_group_destroy.argtypes = [P]
+    L.hxf_comm_create_group.argtypes = [P, P, I, C.POINTER(P)]
+    L.hxf_comm_destroy.argtypes = [P]
+    L.hxf_comm_rank.argtypes = [P]
+    L.hxf_comm_size.argtypes = [P]
+    L.hxf_comm_allreduce_sum.argtypes = [P, P, I64, P]
+    L.hxf_operator_set_partition.argtypes = [P, P, C.POINTER(PartitionDesc)]
+    L.hxf_operator_halo_sum.argtypes = [P, P, I]
     _lib = L
     return L
 
@@ -335,3 +355,85 @@ class Operator:
             "total_time_seconds": rep.total_time_seconds,
         }
         return x, report
+
+
+# ---- partitioned box (include/hxf.h "partitioned box") ----------------------
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * COMM_ID_BYTES)()
+    check(lib().hxf_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class CommGroup:
+    """In-process group: n sub-domains, one host thread each (ctypes drops the GIL)."""
+
+    def __init__(self, nranks: int):
+        self._h = C.c_void_p()
+        check(lib().hxf_comm_group_create(nranks, C.byref(self._h)))
+        self.size = nranks
+
+    def close(self):
+        if self._h:
+            lib().hxf_comm_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Comm:
+    def __init__(self, ctx: Context, *, group: CommGroup = None, rank: int = 0,
+                 nranks: int = 1, unique_id: bytes = None):
+        self.ctx = ctx
+        self._h = C.c_void_p()
+        if group is not None:
+            check(lib().hxf_comm_create_group(ctx.handle, group._h, rank, C.byref(self._h)))
+        else:
+            buf = (C.c_ubyte * COMM_ID_BYTES).from_buffer_copy(unique_id)
+            check(lib().hxf_comm_create_nccl(ctx.handle, nranks, rank, buf, C.byref(self._h)))
+
+    @property
+    def rank(self) -> int:
+        return int(lib().hxf_comm_rank(self._h))
+
+    @property
+    def size(self) -> int:
+        return int(lib().hxf_comm_size(self._h))
+
+    def allreduce_sum(self, t) -> None:
+        """In-place sum of a CUDA float64 tensor across ranks."""
+        check(lib().hxf_comm_allreduce_sum(self._h, t.data_ptr(), t.numel(), None))
+
+    def close(self):
+        if self._h:
+            lib().hxf_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def set_partition(op: Operator, comm: Comm, neighbor) -> None:
+    """neighbor[axis][side] = rank sharing the low (0) / high (1) face plane, -1 = none."""
+    d = PartitionDesc()
+    for a in range(3):
+        for s in range(2):
+            d.neighbor[a][s] = int(neighbor[a][s])
+    check(lib().hxf_operator_set_partition(op._h, comm._h, C.byref(d)))
+    op._comm = comm  # keep the communicator alive with the operator
+
+
+def halo_sum(op: Operator, v):
+    v = _f64(v)
+    vp, space = _ptr(v)
+    check(lib().hxf_operator_halo_sum(op._h, vp, space))
+    return v

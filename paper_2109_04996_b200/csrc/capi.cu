@@ -16,26 +16,13 @@
 #include <string>
 #include <vector>
 
-#include "aux_kernels.h"
-#include "hxf_internal.h"
-#include "pcg_kernels.h"
+#include "capi_internal.h"
 
 namespace {
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 int g_sms = 0;
-
-struct HxfError {
-  int code;
-  std::string msg;
-};
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw HxfError{code, msg}; }
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) fail(HXF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
 
 template <class F>
 int guarded(F&& f) {
@@ -51,30 +38,7 @@ int guarded(F&& f) {
   }
 }
 
-template <class T>
-T* dalloc(size_t n) {
-  void* p = nullptr;
-  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
-  return static_cast<T*>(p);
-}
 
-struct DevVec {
-  double* p = nullptr;
-  size_t n = 0;
-  double* ensure(size_t want) {
-    if (want > n) {
-      if (p) cudaFree(p);
-      p = dalloc<double>(want);
-      n = want;
-    }
-    return p;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-};
 
 void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpy H2D");
@@ -158,74 +122,11 @@ cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams&
   }
 }
 
+void set_last_error(const char* msg) { g_err = msg; }
+
 }  // namespace hxf
 
-using namespace hxf;
 
-struct hxf_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  void* nccl = nullptr;
-  DevVec scratch_a, scratch_b, scratch_c, scratch_d;  // API-surface staging
-};
-
-struct hxf_op {
-  hxf_ctx* ctx = nullptr;
-  int p = 0, q = 0, m = 1, P = 0, Q = 0;
-  int64_t E = 0, n_L = 0;
-  bool interp = false;
-  std::vector<double> B, Dq;  // kernel-parameter matrices
-  double alpha = 0, beta = 0;
-  bool structured = false;
-  int nx = 0, ny = 0, nz = 0;
-  int64_t NX = 0, NY = 0, NZ = 0;
-  int* d_idx = nullptr;
-  int cons_mode = 0;
-  uint32_t* d_mask = nullptr;
-  int64_t ncons = 0;
-  double* d_qd_diff = nullptr;
-  int64_t diff_stride = 0;
-  double* d_qd_mass = nullptr;
-  int64_t mass_stride = 0;
-  double* d_part = nullptr;
-  double *d_B = nullptr, *d_G = nullptr, *d_Bt = nullptr, *d_Gt = nullptr;
-  double *d_bb = nullptr, *d_dd = nullptr, *d_bd = nullptr;
-  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_dinv, w_vpart, w_hist, w_ediag, w_ldiag;
-  PcgState* d_state = nullptr;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;  // cached fixed-iteration PCG graph
-  std::vector<const void*> graph_key;
-  int64_t graph_kernels = 0;
-
-  int64_t size() const { return int64_t(m) * n_L; }
-  Lattice lattice() const {
-    Lattice L;
-    L.p = p;
-    L.S = (p + 1) * (p + 1) * (p + 1);
-    L.E = E;
-    L.n_L = n_L;
-    L.NX = NX;
-    L.NY = NY;
-    L.nx = nx;
-    L.ny = ny;
-    L.nz = nz;
-    return L;
-  }
-  ~hxf_op() {
-    for (void* ptr : {(void*)d_idx, (void*)d_mask, (void*)d_qd_diff, (void*)d_qd_mass,
-                      (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
-                      (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state})
-      if (ptr) cudaFree(ptr);
-    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
-                      &w_ldiag})
-      v->release();
-    for (auto e : ev) cudaEventDestroy(e);
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    if (ev_t0) cudaEventDestroy(ev_t0);
-    if (ev_t1) cudaEventDestroy(ev_t1);
-  }
-};
 
 namespace {
 
@@ -237,8 +138,9 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
 // REDs into it).  PCG (st != nullptr): per-CTA partials of p.(A p) go to
 // dot_part and the last CTA of the last pass derives alpha into *st.
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
-                  int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr) {
-  if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask), "init_y");
+                  int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr,
+                  bool halo = true) {
+  if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask, op->d_own), "init_y");
   OpParams prm{};
   prm.x = x;
   prm.y = y;
@@ -251,6 +153,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.ny = op->ny;
   prm.idx = op->structured ? nullptr : op->d_idx;
   prm.cons_mode = op->cons_mode;
+  prm.bnd_faces = op->bnd_faces;
   prm.cons_mask = op->d_mask;
   prm.stop = stop;
   prm.ablate = ablate_bits();
@@ -273,6 +176,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
     total += grid;
   }
   if (nparts) *nparts = total;
+  if (halo) op_halo_sum(op, y, s);  // partitioned: assemble interface rows (else no-op)
 }
 
 std::vector<int64_t> sorted_unique(const int64_t* v, int64_t n) {
@@ -504,15 +408,40 @@ int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* d, hxf_op** out) 
          "mask upload");
       op->cons_mode = 2;
       if (op->structured) {
-        const int64_t nb = op->n_L - (op->NX - 2) * (op->NY - 2) * (op->NZ - 2);
-        bool boundary = int64_t(cons.size()) == nb && op->NX > 1 && op->NY > 1 && op->NZ > 1;
-        for (size_t i = 0; boundary && i < cons.size(); ++i) {
-          const int64_t c = cons[i], ix = c % op->NX, iy = (c / op->NX) % op->NY,
-                        iz = c / (op->NX * op->NY);
-          boundary = ix == 0 || ix == op->NX - 1 || iy == 0 || iy == op->NY - 1 || iz == 0 ||
-                     iz == op->NZ - 1;
+        // box-face form: the list is exactly the union of some faces of the
+        // lattice (all six: the single-domain BP3-6 case; a subset: a
+        // subdomain of a partitioned box, constrained only on global faces)
+        auto bit = [&](int64_t n) { return (mask[size_t(n >> 5)] >> (n & 31)) & 1u; };
+        const int64_t NX = op->NX, NY = op->NY, NZ = op->NZ;
+        auto face_full = [&](int f) {
+          const int axis = f / 2;
+          const int64_t fixed = (f & 1) ? (axis == 0 ? NX : axis == 1 ? NY : NZ) - 1 : 0;
+          const int64_t na = axis == 0 ? NY : NX, nb = axis == 2 ? NY : NZ;
+          for (int64_t b = 0; b < nb; ++b)
+            for (int64_t a = 0; a < na; ++a) {
+              const int64_t ix = axis == 0 ? fixed : a, iy = axis == 1 ? fixed : (axis == 0 ? a : b),
+                            iz = axis == 2 ? fixed : b;
+              if (!bit(ix + NX * (iy + NY * iz))) return false;
+            }
+          return true;
+        };
+        int faces = 0;
+        for (int f = 0; f < 6; ++f)
+          if (face_full(f)) faces |= 1 << f;
+        OpParams probe{};
+        probe.NX = NX;
+        probe.NY = NY;
+        probe.NZ = NZ;
+        probe.bnd_faces = faces;
+        bool exact = faces != 0;
+        for (size_t i = 0; exact && i < cons.size(); ++i) {
+          const int64_t c = cons[i];
+          exact = on_bnd_face(probe, c % NX, (c / NX) % NY, c / (NX * NY));
         }
-        if (boundary) op->cons_mode = 1;
+        if (exact) {
+          op->cons_mode = 1;
+          op->bnd_faces = faces;
+        }
       }
     }
     if (op->alpha > 0) upload_qdata(op.get(), d->diff_qdata, 6, d->qdata_space, &op->d_qd_diff,
@@ -592,6 +521,10 @@ int hxf_operator_diagonal(hxf_op* op, double* d, hxf_memspace space) {
                        op->d_dd, op->d_bd, op->d_qd_mass, op->mass_stride, op->d_qd_diff,
                        op->diff_stride, op->alpha, op->beta, op->m, op->d_mask, ediag, ldiag, dd),
        "operator_diagonal");
+    if (op_partitioned(op)) {  // one copy of each constrained 1, then assemble
+      op_set_constrained(op, dd, 1.0, s);
+      op_halo_sum(op, dd, s);
+    }
     if (space == HXF_HOST) d2h(d, dd, size_t(op->size()) * 8, s);
     ck(cudaStreamSynchronize(s), "operator_diagonal");
   });
@@ -828,6 +761,8 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     st.limit = limit;
     st.fixed = fixed ? 1 : 0;
     const int* stop = &op->d_state->stop;
+    double* red = reinterpret_cast<double*>(reinterpret_cast<char*>(op->d_state) +
+                                            offsetof(PcgState, red));  // device slots
 
     // (External: inside a captured graph the record is a real timing event)
     bool capturing = false;
@@ -841,24 +776,33 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     auto iteration = [&](int it) {
       int nparts = 0;
       record(op->ev[2 * (it - 1)]);
-      // Ap was preset by the init / direction kernel: no memset pass here
-      device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state);
-      record(op->ev[2 * (it - 1) + 1]);
-      ck(pcg_launch_update(s, op->d_state, it, int64_t(n), dinv, dx, r, p, Ap, vpart, hist),
+      // Ap was preset by the init / direction kernel: no memset pass here;
+      // partitioned: K1 ends with the interface sum-exchange of Ap
+      device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state,
+                   /*halo=*/false);
+      record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
+      op_halo_sum(op, Ap, s);
+      op_allreduce(op, red, 1, s);  // pAp
+      ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, dinv, dx, r, p, Ap, op->d_own,
+                           vpart),
          "pcg update");
-      ck(pcg_launch_direction(s, op->d_state, op->n_L, op->m, dinv, r, p, Ap, op->d_mask, vpart),
+      op_allreduce(op, red + 1, 2, s);  // r.r, r.z
+      ck(pcg_launch_direction(s, op->d_state, it, hist, op->n_L, op->m, dinv, r, p, Ap,
+                              op->d_mask, op->d_own, vpart),
          "pcg direction");
     };
     auto init = [&] {
       ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, db, dd, dinv, dx, r, p, Ap, op->d_mask,
-                         vpart, hist),
+                         op->d_own, vpart),
          "pcg init");
+      op_allreduce(op, red + 4, 2, s);  // b.b, b.z
+      ck(pcg_launch_init_finalize(s, op->d_state, hist), "pcg init");
     };
 
     int launched = 0;
     ck(cudaEventRecord(op->ev_t0, s), "event");
     h2d(op->d_state, &st, sizeof st, s);
-    if (fixed) {
+    if (fixed && op_graph_safe(op)) {
       // benchmark semantics: the whole fixed-iteration solve as one CUDA graph
       // (launch-gap free), captured once per operand set and replayed
       const std::vector<const void*> key = {db, dd, dx, dinv, (const void*)(intptr_t)limit};
@@ -881,6 +825,10 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
       }
       ck(cudaGraphLaunch(op->graph_exec, s), "graph launch");
       count_launch(int(op->graph_kernels));
+      launched = limit;
+    } else if (fixed) {  // host-synchronous communicator: no graph capture
+      init();
+      for (int it = 1; it <= limit; ++it) iteration(it);
       launched = limit;
     } else {
       init();

@@ -1,0 +1,144 @@
+// Internal host-side definitions shared by the C-ABI translation units
+// (capi.cu, dist.cu): error helpers, device allocation, and the context /
+// operator handle structs behind the opaque hxf_ctx / hxf_op.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "aux_kernels.h"
+#include "hxf_internal.h"
+#include "pcg_kernels.h"
+
+namespace hxf {
+struct Comm;  // dist.cu
+}
+
+namespace hxf_detail {
+struct HxfError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw HxfError{code, msg}; }
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HXF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+struct DevVec {
+  double* p = nullptr;
+  size_t n = 0;
+  double* ensure(size_t want) {
+    if (want > n) {
+      if (p) cudaFree(p);
+      p = dalloc<double>(want);
+      n = want;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace hxf_detail
+
+using namespace hxf;
+using namespace hxf_detail;
+
+struct hxf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* nccl = nullptr;
+  DevVec scratch_a, scratch_b, scratch_c, scratch_d;  // API-surface staging
+};
+
+struct hxf_op {
+  hxf_ctx* ctx = nullptr;
+  int p = 0, q = 0, m = 1, P = 0, Q = 0;
+  int64_t E = 0, n_L = 0;
+  bool interp = false;
+  std::vector<double> B, Dq;  // kernel-parameter matrices
+  double alpha = 0, beta = 0;
+  bool structured = false;
+  int nx = 0, ny = 0, nz = 0;
+  int64_t NX = 0, NY = 0, NZ = 0;
+  int* d_idx = nullptr;
+  int cons_mode = 0;
+  int bnd_faces = 0;
+  uint32_t* d_mask = nullptr;
+  int64_t ncons = 0;
+  double* d_qd_diff = nullptr;
+  int64_t diff_stride = 0;
+  double* d_qd_mass = nullptr;
+  int64_t mass_stride = 0;
+  double* d_part = nullptr;
+  double *d_B = nullptr, *d_G = nullptr, *d_Bt = nullptr, *d_Gt = nullptr;
+  double *d_bb = nullptr, *d_dd = nullptr, *d_bd = nullptr;
+  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_dinv, w_vpart, w_hist, w_ediag, w_ldiag;
+  PcgState* d_state = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;  // cached fixed-iteration PCG graph
+  std::vector<const void*> graph_key;
+  int64_t graph_kernels = 0;
+  // partitioned box (hxf_operator_set_partition): the communicator, the
+  // subdomains sharing this lattice's low / high face plane per axis, the
+  // owner mask over scalar nodes (dots) and plane staging buffers
+  hxf::Comm* comm = nullptr;
+  int neighbor[3][2] = {{-1, -1}, {-1, -1}, {-1, -1}};
+  uint32_t* d_own = nullptr;
+  DevVec w_halo;
+
+  int64_t size() const { return int64_t(m) * n_L; }
+  Lattice lattice() const {
+    Lattice L;
+    L.p = p;
+    L.S = (p + 1) * (p + 1) * (p + 1);
+    L.E = E;
+    L.n_L = n_L;
+    L.NX = NX;
+    L.NY = NY;
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    return L;
+  }
+  ~hxf_op() {
+    for (void* ptr : {(void*)d_idx, (void*)d_mask, (void*)d_qd_diff, (void*)d_qd_mass,
+                      (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
+                      (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state, (void*)d_own})
+      if (ptr) cudaFree(ptr);
+    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
+                      &w_ldiag, &w_halo})
+      v->release();
+    for (auto e : ev) cudaEventDestroy(e);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (ev_t0) cudaEventDestroy(ev_t0);
+    if (ev_t1) cudaEventDestroy(ev_t1);
+  }
+};
+
+namespace hxf {
+// dist.cu: interface sum-exchange and all-reduce for partitioned operators
+// (no-ops for a single-domain operator).
+void op_halo_sum(hxf_op* op, double* v, cudaStream_t s);
+void op_allreduce(hxf_op* op, double* dev, int n, cudaStream_t s);
+bool op_partitioned(const hxf_op* op);
+bool op_graph_safe(const hxf_op* op);
+void set_last_error(const char* msg);  // capi.cu: the thread's hxf_last_error()
+void op_set_constrained(hxf_op* op, double* v, double value, cudaStream_t s);
+}  // namespace hxf

@@ -153,15 +153,17 @@ TensorBasis make_basis(int p, const QuadratureRule& quad) {
 }
 
 // ------------------------------------------------------------ mesh
-HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
-  if (nx < 1 || ny < 1 || nz < 1)
-    throw std::invalid_argument("build_mesh: element counts must be >= 1");
-  if (p < 1) throw std::invalid_argument("build_mesh: p must be >= 1");
+namespace {
+// The lattice of the element sub-box [off, off + loc) of a global box of
+// `glob` elements, coordinates evaluated on the global 1-D axes (mesh.cpp:
+// 42-78) so a sub-box mesh is bit-equal to the matching part of the global.
+HexMesh build_box_mesh(std::array<int, 3> glob, std::array<int, 3> off, std::array<int, 3> loc,
+                       int p, Deformation deformation) {
   HexMesh mesh;
-  mesh.dims = {nx, ny, nz};
+  mesh.dims = loc;
   mesh.p = p;
   mesh.deformation = deformation;
-  mesh.nodes_per_axis = {int64_t(nx) * p + 1, int64_t(ny) * p + 1, int64_t(nz) * p + 1};
+  mesh.nodes_per_axis = {int64_t(loc[0]) * p + 1, int64_t(loc[1]) * p + 1, int64_t(loc[2]) * p + 1};
   mesh.n_L = mesh.nodes_per_axis[0] * mesh.nodes_per_axis[1] * mesh.nodes_per_axis[2];
   const std::vector<double> gll = make_quadrature(QuadratureKind::GaussLobattoLegendre, p + 1).points;
   auto axis = [&](int ne) {
@@ -173,9 +175,12 @@ HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
     c.front() = 0.0;
     return c;
   };
-  const auto cx = axis(nx), cy = axis(ny), cz = axis(nz);
+  const auto cx = axis(glob[0]), cy = axis(glob[1]), cz = axis(glob[2]);
   const int64_t NX = mesh.nodes_per_axis[0], NY = mesh.nodes_per_axis[1],
                 NZ = mesh.nodes_per_axis[2];
+  const int64_t GX = int64_t(glob[0]) * p + 1, GY = int64_t(glob[1]) * p + 1,
+                GZ = int64_t(glob[2]) * p + 1;
+  const int64_t ox = int64_t(off[0]) * p, oy = int64_t(off[1]) * p, oz = int64_t(off[2]) * p;
   mesh.coords.assign(size_t(3 * mesh.n_L), 0.0);
   // the sine bump factorises: s(x,y,z) = sin(pi x) sin(pi y) sin(pi z), with
   // the reference's evaluation order ((eps*sx)*sy)*sz kept per node
@@ -187,9 +192,10 @@ HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
   for (int64_t iz = 0; iz < NZ; ++iz)
     for (int64_t iy = 0; iy < NY; ++iy)
       for (int64_t ix = 0; ix < NX; ++ix, ++node) {
-        double x = cx[size_t(ix)], y = cy[size_t(iy)], z = cz[size_t(iz)];
+        const size_t gx = size_t(ox + ix), gy = size_t(oy + iy), gz = size_t(oz + iz);
+        double x = cx[gx], y = cy[gy], z = cz[gz];
         if (deformation == Deformation::Sine) {
-          const double bump = 0.05 * sx[size_t(ix)] * sy[size_t(iy)] * sz[size_t(iz)];
+          const double bump = 0.05 * sx[gx] * sy[gy] * sz[gz];
           x += bump;
           y += bump;
           z += bump;
@@ -197,10 +203,107 @@ HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
         mesh.coords[size_t(node)] = x;
         mesh.coords[size_t(mesh.n_L + node)] = y;
         mesh.coords[size_t(2 * mesh.n_L + node)] = z;
-        if (ix == 0 || ix == NX - 1 || iy == 0 || iy == NY - 1 || iz == 0 || iz == NZ - 1)
+        if (gx == 0 || int64_t(gx) == GX - 1 || gy == 0 || int64_t(gy) == GY - 1 || gz == 0 ||
+            int64_t(gz) == GZ - 1)
           mesh.boundary_nodes.push_back(node);
       }
   return mesh;
+}
+}  // namespace
+
+HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
+  if (nx < 1 || ny < 1 || nz < 1)
+    throw std::invalid_argument("build_mesh: element counts must be >= 1");
+  if (p < 1) throw std::invalid_argument("build_mesh: p must be >= 1");
+  return build_box_mesh({nx, ny, nz}, {0, 0, 0}, {nx, ny, nz}, p, deformation);
+}
+
+// ------------------------------------------------------------ partition
+std::array<int, 3> proc_grid(int nranks, std::array<int, 3> global_dims) {
+  if (nranks < 1) throw std::invalid_argument("proc_grid: nranks must be >= 1");
+  // prime factors, largest first, each onto the axis with the most elements
+  // per rank (ties: x, then y, then z): 2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2
+  std::vector<int> f;
+  for (int n = nranks, d = 2; n > 1;) {
+    if (n % d == 0) {
+      f.push_back(d);
+      n /= d;
+    } else {
+      ++d;
+    }
+  }
+  std::sort(f.rbegin(), f.rend());
+  std::array<int, 3> g{1, 1, 1};
+  for (int k : f) {
+    int best = 0;
+    for (int a = 1; a < 3; ++a)
+      if (double(global_dims[size_t(a)]) / g[size_t(a)] >
+          double(global_dims[size_t(best)]) / g[size_t(best)])
+        best = a;
+    g[size_t(best)] *= k;
+  }
+  return g;
+}
+
+Subdomain make_subdomain(std::array<int, 3> global_dims, int nranks, int rank,
+                         std::optional<std::array<int, 3>> grid) {
+  if (rank < 0 || rank >= nranks) throw std::invalid_argument("make_subdomain: bad rank");
+  Subdomain sd;
+  sd.rank = rank;
+  sd.nranks = nranks;
+  sd.global_dims = global_dims;
+  sd.grid = grid ? *grid : proc_grid(nranks, global_dims);
+  if (sd.grid[0] * sd.grid[1] * sd.grid[2] != nranks)
+    throw std::invalid_argument("make_subdomain: process grid does not match the rank count");
+  sd.coord = {rank % sd.grid[0], (rank / sd.grid[0]) % sd.grid[1], rank / (sd.grid[0] * sd.grid[1])};
+  for (size_t a = 0; a < 3; ++a) {
+    const int G = global_dims[a], g = sd.grid[a], c = sd.coord[a];
+    if (G < g) throw std::invalid_argument("make_subdomain: fewer elements than ranks along an axis");
+    const int base = G / g, extra = G % g;
+    sd.dims[a] = base + (c < extra ? 1 : 0);
+    sd.offset[a] = c * base + std::min(c, extra);
+    std::array<int, 3> lo = sd.coord, hi = sd.coord;
+    lo[a] -= 1;
+    hi[a] += 1;
+    auto rank_of = [&](const std::array<int, 3>& k) {
+      return k[0] + sd.grid[0] * (k[1] + sd.grid[1] * k[2]);
+    };
+    sd.neighbor[a][0] = c > 0 ? rank_of(lo) : -1;
+    sd.neighbor[a][1] = c + 1 < g ? rank_of(hi) : -1;
+  }
+  return sd;
+}
+
+HexMesh build_submesh(const Subdomain& sd, int p, Deformation deformation) {
+  if (p < 1) throw std::invalid_argument("build_mesh: p must be >= 1");
+  return build_box_mesh(sd.global_dims, sd.offset, sd.dims, p, deformation);
+}
+
+std::vector<int64_t> global_node_ids(const Subdomain& sd, int p) {
+  const int64_t NX = int64_t(sd.dims[0]) * p + 1, NY = int64_t(sd.dims[1]) * p + 1,
+                NZ = int64_t(sd.dims[2]) * p + 1;
+  const int64_t GX = int64_t(sd.global_dims[0]) * p + 1, GY = int64_t(sd.global_dims[1]) * p + 1;
+  std::vector<int64_t> ids(size_t(NX * NY * NZ));
+  size_t i = 0;
+  for (int64_t iz = 0; iz < NZ; ++iz)
+    for (int64_t iy = 0; iy < NY; ++iy)
+      for (int64_t ix = 0; ix < NX; ++ix)
+        ids[i++] = (int64_t(sd.offset[0]) * p + ix) +
+                   GX * ((int64_t(sd.offset[1]) * p + iy) + GY * (int64_t(sd.offset[2]) * p + iz));
+  return ids;
+}
+
+std::vector<uint8_t> owned_nodes(const Subdomain& sd, int p) {
+  const int64_t NX = int64_t(sd.dims[0]) * p + 1, NY = int64_t(sd.dims[1]) * p + 1,
+                NZ = int64_t(sd.dims[2]) * p + 1;
+  const bool lx = sd.neighbor[0][0] >= 0, ly = sd.neighbor[1][0] >= 0, lz = sd.neighbor[2][0] >= 0;
+  std::vector<uint8_t> own(size_t(NX * NY * NZ));
+  size_t i = 0;
+  for (int64_t iz = 0; iz < NZ; ++iz)
+    for (int64_t iy = 0; iy < NY; ++iy)
+      for (int64_t ix = 0; ix < NX; ++ix)
+        own[i++] = !((lx && ix == 0) || (ly && iy == 0) || (lz && iz == 0));
+  return own;
 }
 
 // ------------------------------------------------------------ device
@@ -235,6 +338,45 @@ void DeviceBuffer::download(double* dst, size_t count) const {
   check(hxf_memcpy(dev_->ctx(), dst, ptr_, uint64_t(count) * 8, 1));
 }
 
+std::string Communicator::unique_id() {
+  std::string id(HXF_COMM_ID_BYTES, '\0');
+  check(hxf_comm_unique_id(reinterpret_cast<unsigned char*>(id.data())));
+  return id;
+}
+std::shared_ptr<Communicator> Communicator::nccl(int device, int nranks, int rank,
+                                                 const std::string& id) {
+  if (id.size() != HXF_COMM_ID_BYTES) throw std::invalid_argument("nccl: bad unique id length");
+  std::shared_ptr<Communicator> c(new Communicator());
+  c->dev_ = Device::get(device);
+  check(hxf_comm_create_nccl(c->dev_->ctx(), nranks, rank,
+                             reinterpret_cast<const unsigned char*>(id.data()), &c->comm_));
+  return c;
+}
+std::vector<std::shared_ptr<Communicator>> Communicator::group(const std::vector<int>& devices) {
+  hxf_comm_group* g = nullptr;
+  check(hxf_comm_group_create(int(devices.size()), &g));
+  std::shared_ptr<hxf_comm_group> shared(g, [](hxf_comm_group* p) { hxf_comm_group_destroy(p); });
+  std::vector<std::shared_ptr<Communicator>> out;
+  for (size_t r = 0; r < devices.size(); ++r) {
+    std::shared_ptr<Communicator> c(new Communicator());
+    c->dev_ = std::make_shared<Device>(devices[r]);  // own context + stream per sub-domain
+    c->group_ = shared;
+    check(hxf_comm_create_group(c->dev_->ctx(), g, int(r), &c->comm_));
+    out.push_back(c);
+  }
+  return out;
+}
+Communicator::~Communicator() {
+  if (comm_) hxf_comm_destroy(comm_);
+}
+double Communicator::allreduce_sum(double v) const {
+  DeviceBuffer b(dev_, 1);
+  b.upload(&v, 1);
+  check(hxf_comm_allreduce_sum(comm_, b.data(), 1, nullptr));
+  b.download(&v, 1);
+  return v;
+}
+
 Operator::Operator(std::shared_ptr<Device> dev, const hxf_operator_desc& desc) : dev_(std::move(dev)) {
   check(hxf_operator_create(dev_->ctx(), &desc, &op_));
   size_ = hxf_operator_size(op_);
@@ -249,6 +391,12 @@ void Operator::apply_device(const double* x, double* y, void* stream) const {
   check(hxf_operator_apply(op_, x, y, HXF_DEVICE, stream));
 }
 void Operator::diagonal_device(double* d) const { check(hxf_operator_diagonal(op_, d, HXF_DEVICE)); }
+void Operator::set_partition(const Communicator& comm, const Subdomain& sd) const {
+  hxf_partition_desc d{};
+  for (int a = 0; a < 3; ++a)
+    for (int s = 0; s < 2; ++s) d.neighbor[a][s] = sd.neighbor[size_t(a)][size_t(s)];
+  check(hxf_operator_set_partition(op_, comm.handle(), &d));
+}
 
 SolveReport Operator::pcg(const double* b, const double* diag, const hxf_pcg_options& o, double* x,
                           hxf_memspace space) const {
@@ -351,11 +499,18 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
   auto prob = std::make_unique<BpProblem>();
   prob->config = config;
   prob->m = bp_components(config.bp);
-  prob->device = Device::get(config.device);
+  const Communicator* comm = config.comm.get();
+  prob->device = comm ? comm->device() : Device::get(config.device);
   auto& dev = prob->device;
   const int q = bp_quadrature_points(config.bp, config.p);
-  prob->mesh = build_mesh(config.dims[0], config.dims[1], config.dims[2], config.p,
-                          config.deformation);
+  if (comm) {
+    prob->sub = make_subdomain(config.dims, comm->size(), comm->rank(), config.proc_grid);
+    prob->mesh = build_submesh(prob->sub, config.p, config.deformation);
+  } else {
+    prob->sub = make_subdomain(config.dims, 1, 0);
+    prob->mesh = build_mesh(config.dims[0], config.dims[1], config.dims[2], config.p,
+                            config.deformation);
+  }
   prob->basis = make_basis(config.p, make_quadrature(bp_quadrature_kind(config.bp), q));
   const HexMesh& mesh = prob->mesh;
   const int64_t n_L = mesh.n_L;
@@ -391,6 +546,7 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
     d.mass_qdata = mass_qd.data();
     d.beta = 1.0;
     Operator mass_op(dev, d);
+    if (comm) mass_op.set_partition(*comm, prob->sub);  // assembled across interfaces
     mass_op.apply_host(f.data(), prob->rhs.data());
   }
   for (int c = 0; c < m; ++c)
@@ -404,7 +560,9 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
   d.constrained = prob->constrained.data();
   d.n_constrained = int64_t(prob->constrained.size());
   prob->op = std::make_unique<Operator>(dev, d);
-  prob->n_dofs = int64_t(m) * (n_L - int64_t(prob->constrained.size()));
+  if (comm) prob->op->set_partition(*comm, prob->sub);
+  prob->n_dofs_local = int64_t(m) * (n_L - int64_t(prob->constrained.size()));
+  prob->n_dofs = bp_dof_count(config.bp, config.p, config.dims);  // global
   prob->d_rhs = DeviceBuffer(dev, size_t(m) * n_L);
   prob->d_rhs.upload(prob->rhs.data(), prob->rhs.size());
   prob->d_diag = DeviceBuffer(dev, size_t(m) * n_L);
@@ -429,7 +587,7 @@ BpSolveResult solve_bp(BpProblem& problem, bool jacobi) {
 // l2_error (bench.cpp:139-189): Gauss q=p+2 rule, element-wise interpolation.
 double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
                 const std::function<double(double, double, double)>& exact,
-                std::shared_ptr<Device> dev) {
+                std::shared_ptr<Device> dev, const Communicator* comm) {
   const int p = mesh.p, n1 = p + 1, q = p + 2;
   const TensorBasis eb = make_basis(p, make_quadrature(QuadratureKind::GaussLegendre, q));
   const int64_t E = mesh.num_elements(), n_L = mesh.n_L;
@@ -478,6 +636,7 @@ double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
     }
     for (int i = 0; i < nq; ++i) err2 += wdet[size_t(e * nq + i)] * diff2[size_t(i)];
   }
+  if (comm) err2 = comm->allreduce_sum(err2);
   return std::sqrt(err2);
 }
 
@@ -508,7 +667,7 @@ BenchRecord run_bench(const BpConfig& config) {
   rec.q = prob->basis.q;
   rec.E = prob->mesh.num_elements();
   rec.n = prob->n_dofs;
-  rec.P = config.threads;
+  rec.P = config.comm ? config.comm->size() : config.threads;
   rec.iterations = iterations;
   rec.seconds = seconds;
   rec.dofs_rate = double(rec.n) * rec.iterations / rec.seconds;

@@ -57,6 +57,27 @@ struct HexMesh {
 };
 HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation = Deformation::None);
 
+// ---- partitioned box (no reference counterpart) -----------
+// The global element box is split into a grid of sub-boxes, one per rank,
+// rank = cx + gx (cy + gy cz).  Each sub-box keeps its own lexicographic
+// node lattice (interface planes duplicated); global_node_ids maps it back to
+// the global numbering of build_mesh bit-exactly.
+std::array<int, 3> proc_grid(int nranks, std::array<int, 3> global_dims);
+struct Subdomain {
+  int rank = 0, nranks = 1;
+  std::array<int, 3> grid{1, 1, 1}, coord{0, 0, 0}, global_dims{1, 1, 1}, offset{0, 0, 0},
+      dims{1, 1, 1};
+  std::array<std::array<int, 2>, 3> neighbor{{{-1, -1}, {-1, -1}, {-1, -1}}};
+};
+Subdomain make_subdomain(std::array<int, 3> global_dims, int nranks, int rank,
+                         std::optional<std::array<int, 3>> grid = std::nullopt);
+// The sub-box's mesh: coordinates taken from the global lattice (bit-equal),
+// boundary_nodes = nodes on the GLOBAL boundary only.
+HexMesh build_submesh(const Subdomain& sd, int p, Deformation deformation = Deformation::None);
+std::vector<int64_t> global_node_ids(const Subdomain& sd, int p);
+// 1 where this sub-box owns the node (not on a low interface plane)
+std::vector<uint8_t> owned_nodes(const Subdomain& sd, int p);
+
 // ---- device context -------------------------------------------------------
 class Device {
  public:
@@ -69,6 +90,29 @@ class Device {
 
  private:
   hxf_ctx* ctx_ = nullptr;
+};
+
+// Communicator for a partitioned problem (hxf_comm): NCCL with one rank per
+// GPU, or an in-process group (one host thread and one context per rank).
+class Communicator {
+ public:
+  static std::string unique_id();  // HXF_COMM_ID_BYTES bytes (rank 0 makes it)
+  static std::shared_ptr<Communicator> nccl(int device, int nranks, int rank, const std::string& id);
+  static std::vector<std::shared_ptr<Communicator>> group(const std::vector<int>& devices);
+  ~Communicator();
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  hxf_comm* handle() const { return comm_; }
+  int rank() const { return hxf_comm_rank(comm_); }
+  int size() const { return hxf_comm_size(comm_); }
+  const std::shared_ptr<Device>& device() const { return dev_; }
+  double allreduce_sum(double v) const;  // host scalar through the device
+
+ private:
+  Communicator() = default;
+  std::shared_ptr<Device> dev_;
+  std::shared_ptr<hxf_comm_group> group_;
+  hxf_comm* comm_ = nullptr;
 };
 
 // Device buffer owned by a Device context.
@@ -122,6 +166,9 @@ struct BpConfig {
   double tol_rel = 1e-8;
   int max_iter = 2000;
   int device = 0;
+  // partitioned: dims are the GLOBAL element counts, this rank builds its sub-box
+  std::shared_ptr<Communicator> comm;
+  std::optional<std::array<int, 3>> proc_grid;
 };
 
 struct SolveReport {
@@ -144,6 +191,7 @@ class Operator {
   void apply_host(const double* x, double* y) const;
   void apply_device(const double* x, double* y, void* stream = nullptr) const;
   void diagonal_device(double* d) const;
+  void set_partition(const Communicator& comm, const Subdomain& sd) const;
   SolveReport pcg(const double* b, const double* diag, const hxf_pcg_options& o, double* x,
                   hxf_memspace space) const;
 
@@ -163,6 +211,8 @@ struct BpProblem {
   std::vector<double> rhs;          // B f, constrained entries zeroed
   std::vector<double> exact_nodal;  // nodal interpolant of u*
   std::shared_ptr<Device> device;
+  Subdomain sub;  // whole box unless config.comm is set
+  int64_t n_dofs_local = 0;
   std::unique_ptr<Operator> op;
   DeviceBuffer d_rhs, d_diag, d_x, d_b;
   bool diag_ready = false;
@@ -178,9 +228,10 @@ struct BpSolveResult {
 };
 BpSolveResult solve_bp(BpProblem& problem, bool jacobi = true);
 
+// comm: sum the squared error over sub-boxes (partitioned problems)
 double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
                 const std::function<double(double, double, double)>& exact,
-                std::shared_ptr<Device> dev);
+                std::shared_ptr<Device> dev, const Communicator* comm = nullptr);
 
 struct BenchRecord {
   std::string bp;

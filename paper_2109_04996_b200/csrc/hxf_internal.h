@@ -14,8 +14,12 @@ enum PcgError { PCG_OK = 0, PCG_ERR_RHS = 1, PCG_ERR_APPLY_NAN = 2, PCG_ERR_INDE
                 PCG_ERR_RESID = 4 };
 
 // Device-resident PCG scalars (pcg_kernels.cu, pcg_device.cuh).
+// red[] holds this rank's reduction results; on a partitioned problem they
+// are all-reduced in place between kernels ([0] pAp, [1] r.r, [2] r.z,
+// [3] constrained p.p (owned rows), [4] b.b, [5] b.z).
 struct PcgState {
-  double rho, pap, alpha, beta, norm_b, target, res, tol, cons_pp;
+  double red[8];
+  double rho, pap, alpha, beta, norm_b, target, res, tol;
   int it, stop, converged, error, limit, fixed;
   unsigned int counter[4];  // last-block counters: K1, update, direction, init
 };
@@ -38,7 +42,8 @@ struct OpParams {
   int64_t NX, NY, NZ;        // structured-box lattice
   int nx, ny;                // elements per axis (x, y)
   const int* idx;            // int32 E x P^3 table, or nullptr (structured box)
-  int cons_mode;             // 0 none, 1 box boundary, 2 bitmask
+  int cons_mode;             // 0 none, 1 box faces (bnd_faces), 2 bitmask
+  int bnd_faces;             // mode 1: bit 2d / 2d+1 = low / high face of axis d constrained
   const uint32_t* cons_mask; // n_L bits (mode 2)
   double* dot_partials;      // per-CTA partial of x_masked . y, or nullptr
   const int* stop;           // device flag: skip the whole kernel when set (PCG)
@@ -47,6 +52,13 @@ struct OpParams {
   const double* D;           // device copy of the 1-D derivative matrix (collocated path)
   PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
 };
+
+// Is lattice node (ix, iy, iz) on a constrained face of the box (mode 1)?
+__host__ __device__ inline bool on_bnd_face(const OpParams& p, int64_t ix, int64_t iy, int64_t iz) {
+  const int f = p.bnd_faces;
+  return (ix == 0 && (f & 1)) || (ix == p.NX - 1 && (f & 2)) || (iy == 0 && (f & 4)) ||
+         (iy == p.NY - 1 && (f & 8)) || (iz == 0 && (f & 16)) || (iz == p.NZ - 1 && (f & 32));
+}
 
 // Launch the fused operator kernel instance for (P, Q, NC, interp, qk);
 // returns cudaErrorNotSupported for an uninstantiated combination.

@@ -122,10 +122,7 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
         for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int64_t x = ix + h, z = iz + kk;
-            if (x == 0 || x == prm.NX - 1 || iy == 0 || iy == prm.NY - 1 || z == 0 ||
-                z == prm.NZ - 1)
-              q.cmask |= 1u << (2 * kk + h);
+            if (on_bnd_face(prm, ix + h, iy, iz + kk)) q.cmask |= 1u << (2 * kk + h);
           }
       }
     }

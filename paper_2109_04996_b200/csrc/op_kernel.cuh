@@ -181,8 +181,7 @@ __global__ void __launch_bounds__(T::NT)
         const int64_t ix = ex * (P - 1) + i, iy = ey * (P - 1) + j, iz = ez * (P - 1) + k;
         node = ix + prm.NX * (iy + prm.NY * iz);
         if (prm.cons_mode == 1)
-          cons = ix == 0 || ix == prm.NX - 1 || iy == 0 || iy == prm.NY - 1 || iz == 0 ||
-                 iz == prm.NZ - 1;
+          cons = on_bnd_face(prm, ix, iy, iz);
         else if (prm.cons_mode == 2)
           cons = (prm.cons_mask[node >> 5] >> (node & 31)) & 1u;
         else

@@ -178,9 +178,9 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       const int64_t ix = ex * (P - 1) + la, iy = ey * (P - 1) + lb, iz = ez * (P - 1);
       g.key = ix + prm.NX * iy + NXY * iz;
       if (T::GM == 0 && prm.cons_mode == 1) {
-        if (ix == 0 || ix == prm.NX - 1 || iy == 0 || iy == prm.NY - 1) g.cmask = (1u << P) - 1;
-        if (iz == 0) g.cmask |= 1u;
-        if (iz + P - 1 == prm.NZ - 1) g.cmask |= 1u << (P - 1);
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          if (on_bnd_face(prm, ix, iy, iz + k)) g.cmask |= 1u << k;
       }
     }
     if (T::GM == 1 && prm.cons_mode == 2) {

@@ -29,8 +29,9 @@ __device__ __forceinline__ double pcg_sum_partials(const double* part, int n, do
   return block_sum<NT>(s, scratch);
 }
 
-// K1 epilogue: publish this CTA's p.(A p) partial; the last CTA derives
-// alpha = rho / pAp with the reference's checks (pcg.cpp:74-82).
+// K1 epilogue: publish this CTA's p.(A p) partial; the last CTA sums all
+// partials in a fixed order and adds the constrained rows' p.p (A p = p
+// there): red[0] = this rank's pAp, all-reduced across ranks if partitioned.
 template <int NT>
 __device__ __forceinline__ void pcg_alpha_epilogue(const PcgAlphaFin& f, double* scratch) {
   if (!f.st) return;
@@ -38,20 +39,8 @@ __device__ __forceinline__ void pcg_alpha_epilogue(const PcgAlphaFin& f, double*
   // partials of earlier passes (f.nparts) followed by this launch's CTAs
   const double s = pcg_sum_partials<NT>(f.parts, f.nparts + (int)gridDim.x, scratch);
   if (threadIdx.x == 0) {
-    PcgState* st = f.st;
-    st->counter[0] = 0;
-    const double pap = s + st->cons_pp;
-    st->pap = pap;
-    if (!isfinite(pap)) {
-      st->error = PCG_ERR_APPLY_NAN;
-      st->stop = 1;
-    } else if (pap <= 0.0) {
-      if (st->rho == 0.0) st->converged = 1;
-      else st->error = PCG_ERR_INDEFINITE;
-      st->stop = 1;
-    } else {
-      st->alpha = st->rho / pap;
-    }
+    f.st->counter[0] = 0;
+    f.st->red[0] = s + f.st->red[3];
   }
 }
 

@@ -2,19 +2,23 @@
 //
 // Restates the reference recurrence (proj/src/pcg.cpp:24-115) with every
 // scalar kept on the device, three launches per iteration:
-//   K1      Ap += A p over free rows (op_pencil.cuh / op_kernel.cuh); its last
-//           CTA sums the p.(A p) partials + the constrained part and derives
-//           alpha with the reference's checks (pcg.cpp:74-82)
-//   update  x += alpha p, r -= alpha Ap; last CTA: ||r||, history,
-//           convergence / limit (pcg.cpp:90-99), beta = rho' / rho
-//   dir     p = r/d + beta p; Ap = (constrained ? p : 0), the next RED
-//           target; last CTA: sum of p^2 on constrained rows
-// Each reduction is per-CTA partials over a fixed grid summed in a fixed
-// order by the CTA that finishes last ("last CTA" pattern, pcg_device.cuh):
-// no extra launches, bitwise reproducible run to run (the reference's
-// dot_deterministic, parallel.cpp:69-106, plays that role).  A kernel reads
-// the stop flag only at its start; it is written only by a last CTA.
-
+//   K1      Ap += A p over free rows (op_dmma / op_pencil / op_kernel); its
+//           last CTA writes this rank's pAp into red[0]
+//   update  every CTA derives alpha = rho / pAp from red[0] with the
+//           reference's checks (pcg.cpp:74-82); x += alpha p, r -= alpha Ap;
+//           last CTA: red[1] = r.r, red[2] = r.(r/d) over owned rows
+//   dir     every CTA derives ||r||, convergence / limit (pcg.cpp:90-99) and
+//           beta = rho' / rho from red[1..2]; p = r/d + beta p;
+//           Ap = (constrained & owned ? p : 0), the next RED target; last CTA
+//           records the iteration and red[3] = sum of p^2 over owned
+//           constrained rows
+// On a partitioned problem red[] is all-reduced across ranks between the
+// kernels (dist.cu); on one GPU the same kernels run back to back.  Each
+// reduction is per-CTA partials over a fixed grid summed in a fixed order by
+// the CTA that finishes last (pcg_device.cuh): bitwise reproducible run to
+// run (the reference's dot_deterministic, parallel.cpp:69-106, plays that
+// role).  Scalars are read at kernel start and written only by the last CTA
+// (or, on an early stop, by CTA 0 — nothing reads them later in that kernel).
 #include "pcg_device.cuh"
 #include "pcg_kernels.h"
 
@@ -23,19 +27,26 @@ namespace hxf {
 namespace {
 constexpr int VT = 256;
 
+__device__ __forceinline__ uint32_t bit_of(const uint32_t* mask, int64_t node) {
+  return (mask[node >> 5] >> (node & 31)) & 1u;
+}
 __device__ __forceinline__ bool is_cons(const uint32_t* mask, int64_t node) {
-  return mask && ((mask[node >> 5] >> (node & 31)) & 1u);
+  return mask && bit_of(mask, node);
+}
+// owned rows weigh 1 in dots (no owner mask: everything is owned)
+__device__ __forceinline__ double owned_w(const uint32_t* own, int64_t node) {
+  return (!own || bit_of(own, node)) ? 1.0 : 0.0;
 }
 }  // namespace
 
 __global__ void __launch_bounds__(VT)
     pcg_init_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ b,
                     const double* __restrict__ d, double* __restrict__ dinv,
-                    double* __restrict__ x, double* __restrict__ r,
-                    double* __restrict__ p, double* __restrict__ Ap, const uint32_t* cons_mask,
-                    double* part, double* hist) {
+                    double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+                    double* __restrict__ Ap, const uint32_t* cons_mask, const uint32_t* own,
+                    double* part) {
   __shared__ double scratch[VT / 32];
-  double rr = 0.0, rz = 0.0, cc = 0.0;
+  double bb = 0.0, bz = 0.0, cc = 0.0;
   const int64_t stride = (int64_t)gridDim.x * VT;
   for (int c = 0; c < m; ++c) {
     for (int64_t node = (int64_t)blockIdx.x * VT + threadIdx.x; node < n_L; node += stride) {
@@ -47,18 +58,21 @@ __global__ void __launch_bounds__(VT)
         dinv[i] = di;
         zi = bi * di;
       }
+      const double w = owned_w(own, node);
       const bool cons = is_cons(cons_mask, node);
       x[i] = 0.0;
       r[i] = bi;
       p[i] = zi;
-      Ap[i] = cons ? zi : 0.0;  // operator kernels skip constrained rows (A p = p there)
-      rr += bi * bi;
-      rz += bi * zi;
-      if (cons) cc += zi * zi;
+      // operator kernels skip constrained rows (A p = p there); one owner
+      // presets it so an interface sum-exchange leaves exactly p
+      Ap[i] = (cons && w != 0.0) ? zi : 0.0;
+      bb += w * bi * bi;
+      bz += w * bi * zi;
+      if (cons) cc += w * zi * zi;
     }
   }
-  const double s0 = block_sum<VT>(rr, scratch);
-  const double s1 = block_sum<VT>(rz, scratch);
+  const double s0 = block_sum<VT>(bb, scratch);
+  const double s1 = block_sum<VT>(bz, scratch);
   const double s2 = block_sum<VT>(cc, scratch);
   const int g = gridDim.x;
   if (threadIdx.x == 0) {
@@ -67,86 +81,121 @@ __global__ void __launch_bounds__(VT)
     part[2 * g + blockIdx.x] = s2;
   }
   if (!pcg_last_cta(&st->counter[3])) return;
-  const double tr = pcg_sum_partials<VT>(part, g, scratch);
+  const double tb = pcg_sum_partials<VT>(part, g, scratch);
   const double tz = pcg_sum_partials<VT>(part + g, g, scratch);
   const double tc = pcg_sum_partials<VT>(part + 2 * g, g, scratch);
   if (threadIdx.x == 0) {
     st->counter[3] = 0;
-    const double norm_b = sqrt(tr);  // pcg.cpp:53-64
-    st->it = 0;
-    st->converged = 0;
-    st->error = 0;
-    st->stop = 0;
-    st->cons_pp = tc;
-    if (!isfinite(norm_b)) {
-      st->error = PCG_ERR_RHS;
-      st->stop = 1;
-      return;
-    }
-    hist[0] = norm_b;
-    st->norm_b = norm_b;
-    st->res = norm_b;
-    st->target = st->tol * norm_b;
-    if (norm_b == 0.0) {
-      st->converged = 1;
-      st->stop = 1;
-      return;
-    }
-    st->rho = tz;
+    st->red[3] = tc;  // stays local: K1 adds it before its own all-reduce
+    st->red[4] = tb;
+    st->red[5] = tz;
   }
 }
 
-// Iteration `it` (1-based): x += alpha p, r -= alpha Ap; r.r, r.z partials;
-// the last CTA decides convergence and beta.  VEC: 16-byte aligned vectors,
-// two entries per 128-bit access, two pairs per loop trip.
-template <bool VEC>
-__global__ void __launch_bounds__(VT, 4)
-    pcg_update_kernel(PcgState* st, int it, int64_t n, const double* __restrict__ d,
+// After (optionally) all-reducing red[4..5]: ||b||, rho, checks (pcg.cpp:53-64).
+__global__ void pcg_init_finalize(PcgState* st, double* hist) {
+  if (threadIdx.x != 0) return;
+  const double norm_b = sqrt(st->red[4]);
+  st->it = 0;
+  st->converged = 0;
+  st->error = 0;
+  st->stop = 0;
+  if (!isfinite(norm_b)) {
+    st->error = PCG_ERR_RHS;
+    st->stop = 1;
+    return;
+  }
+  hist[0] = norm_b;
+  st->norm_b = norm_b;
+  st->res = norm_b;
+  st->target = st->tol * norm_b;
+  if (norm_b == 0.0) {
+    st->converged = 1;
+    st->stop = 1;
+    return;
+  }
+  st->rho = st->red[5];
+}
+
+// Iteration `it` (1-based).  VEC: 16-byte aligned vectors, even n_L, two
+// entries per 128-bit access, two pairs per loop trip.  OWN: owner-weighted
+// dots (partitioned); a separate instantiation keeps the single-domain loop
+// within 64 registers.
+template <bool VEC, bool OWN>
+__global__ void __launch_bounds__(VT, OWN ? 3 : 4)
+    pcg_update_kernel(PcgState* st, int it, int64_t n_L, int m, const double* __restrict__ d,
                       double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                      const double* __restrict__ Ap, double* part, double* hist) {
+                      const double* __restrict__ Ap, const uint32_t* own, double* part) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double alpha = st->alpha;
+  const double pap = st->red[0];
+  const double rho = st->rho;
+  // pcg.cpp:74-82
+  if (!isfinite(pap) || pap <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pap = pap;
+      if (!isfinite(pap)) st->error = PCG_ERR_APPLY_NAN;
+      else if (rho == 0.0) st->converged = 1;
+      else st->error = PCG_ERR_INDEFINITE;
+      st->stop = 1;
+    }
+    return;
+  }
+  const double alpha = rho / pap;
   double rr = 0.0, rz = 0.0;
   const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
-  auto one = [&](int64_t i) {
-    x[i] += alpha * p[i];
-    const double ri = r[i] - alpha * Ap[i];
-    r[i] = ri;
-    rr += ri * ri;
-    rz += ri * (d ? ri * d[i] : ri);  // d holds 1/diag here
-  };
-  if constexpr (VEC) {
-    const int64_t n2 = n / 2;
-    auto two = [&](int64_t k, double2 xv, double2 pv, double2 rv, double2 av, double2 dv) {
-      xv.x += alpha * pv.x;
-      xv.y += alpha * pv.y;
-      rv.x -= alpha * av.x;
-      rv.y -= alpha * av.y;
-      reinterpret_cast<double2*>(x)[k] = xv;
-      reinterpret_cast<double2*>(r)[k] = rv;
-      rr += rv.x * rv.x + rv.y * rv.y;
-      rz += rv.x * (rv.x * dv.x) + rv.y * (rv.y * dv.y);  // dv = 1/diag (or 1)
-    };
-    const double2* x2 = reinterpret_cast<const double2*>(x);
-    const double2* p2 = reinterpret_cast<const double2*>(p);
-    const double2* r2 = reinterpret_cast<const double2*>(r);
-    const double2* a2 = reinterpret_cast<const double2*>(Ap);
-    const double2* d2 = reinterpret_cast<const double2*>(d);
-    const double2 one2 = make_double2(1.0, 1.0);
-    int64_t k = tid;
-    for (; k + stride < n2; k += 2 * stride) {
-      const int64_t k1 = k + stride;
-      const double2 xa = x2[k], pa = p2[k], ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
-      const double2 xb = x2[k1], pb = p2[k1], rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
-      two(k, xa, pa, ra, aa, da);
-      two(k1, xb, pb, rb, ab, db);
+  // without an owner mask nothing depends on the node: one flat pass
+  const int mc = OWN ? m : 1;
+  if constexpr (!OWN) n_L *= m;
+  for (int c = 0; c < mc; ++c) {
+    const int64_t o = c * n_L;
+    if constexpr (VEC) {
+      const int64_t h = n_L / 2;
+      double2* x2 = reinterpret_cast<double2*>(x + o);
+      double2* r2 = reinterpret_cast<double2*>(r + o);
+      const double2* p2 = reinterpret_cast<const double2*>(p + o);
+      const double2* a2 = reinterpret_cast<const double2*>(Ap + o);
+      const double2* d2 = reinterpret_cast<const double2*>(d + o);
+      const double2 one2 = make_double2(1.0, 1.0);
+      auto two = [&](int64_t k, double2 xv, double2 pv, double2 rv, double2 av, double2 dv) {
+        xv.x += alpha * pv.x;
+        xv.y += alpha * pv.y;
+        rv.x -= alpha * av.x;
+        rv.y -= alpha * av.y;
+        x2[k] = xv;
+        r2[k] = rv;
+        const int64_t node = 2 * k;
+        if constexpr (OWN) {
+          const uint32_t wb = (own[node >> 5] >> (node & 31)) & 3u;
+          const double w0 = (wb & 1u) ? 1.0 : 0.0, w1 = (wb & 2u) ? 1.0 : 0.0;
+          rr += w0 * rv.x * rv.x + w1 * rv.y * rv.y;
+          rz += w0 * rv.x * (rv.x * dv.x) + w1 * rv.y * (rv.y * dv.y);  // dv = 1/diag (or 1)
+        } else {
+          rr += rv.x * rv.x + rv.y * rv.y;
+          rz += rv.x * (rv.x * dv.x) + rv.y * (rv.y * dv.y);
+        }
+      };
+      int64_t k = tid;
+      for (; k + stride < h; k += 2 * stride) {
+        const int64_t k1 = k + stride;
+        const double2 xa = x2[k], pa = p2[k], ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
+        const double2 xb = x2[k1], pb = p2[k1], rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
+        two(k, xa, pa, ra, aa, da);
+        two(k1, xb, pb, rb, ab, db);
+      }
+      if (k < h) two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
+    } else {
+      for (int64_t node = tid; node < n_L; node += stride) {
+        const int64_t i = o + node;
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * Ap[i];
+        r[i] = ri;
+        const double w = OWN ? owned_w(own, node) : 1.0;
+        rr += w * ri * ri;
+        rz += w * ri * (d ? ri * d[i] : ri);  // d holds 1/diag here
+      }
     }
-    if (k < n2) two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
-    if ((n & 1) && tid == 0) one(n - 1);
-  } else {
-    for (int64_t i = tid; i < n; i += stride) one(i);
   }
   const double s0 = block_sum<VT>(rr, scratch);
   const double s1 = block_sum<VT>(rz, scratch);
@@ -160,37 +209,44 @@ __global__ void __launch_bounds__(VT, 4)
   const double trz = pcg_sum_partials<VT>(part + g, g, scratch);
   if (threadIdx.x == 0) {
     st->counter[1] = 0;
-    // pcg.cpp:90-107
-    const double res = sqrt(trr);
-    if (!isfinite(res)) {
-      st->error = PCG_ERR_RESID;
-      st->stop = 1;
-      return;
-    }
-    st->it = it;
-    st->res = res;
-    hist[it] = res;
-    const bool conv = res <= st->target;
-    if (conv) st->converged = 1;
-    if ((conv && !st->fixed) || it == st->limit || res == 0.0) {
-      st->stop = 1;
-      return;
-    }
-    st->beta = trz / st->rho;
-    st->rho = trz;
+    st->pap = pap;
+    st->alpha = alpha;
+    st->red[1] = trr;
+    st->red[2] = trz;
   }
 }
 
-// p = z + beta p, Ap preset; last CTA sums p^2 over constrained rows.
-// VEC: 16-byte aligned vectors and an even component stride n_L.
+// Iteration `it`: residual / convergence from red[1..2] (pcg.cpp:90-107);
+// p = z + beta p, Ap preset.  VEC: as for the update kernel.
 template <bool VEC>
 __global__ void __launch_bounds__(VT, 4)
-    pcg_direction_kernel(PcgState* st, int64_t n_L, int m, const double* __restrict__ d,
-                         const double* __restrict__ r, double* __restrict__ p,
-                         double* __restrict__ Ap, const uint32_t* cons_mask, double* part) {
+    pcg_direction_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
+                         const double* __restrict__ d, const double* __restrict__ r,
+                         double* __restrict__ p, double* __restrict__ Ap,
+                         const uint32_t* cons_mask, const uint32_t* own, double* part) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
-  const double beta = st->beta;
+  const double rr = st->red[1], rz = st->red[2];
+  const double res = sqrt(rr);
+  const double rho = st->rho;
+  const bool bad = !isfinite(res);
+  const bool conv = res <= st->target;
+  const bool stop = bad || (conv && !st->fixed) || it == st->limit || res == 0.0;
+  if (stop) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (bad) {
+        st->error = PCG_ERR_RESID;
+      } else {
+        st->it = it;
+        st->res = res;
+        hist[it] = res;
+        if (conv) st->converged = 1;
+      }
+      st->stop = 1;
+    }
+    return;
+  }
+  const double beta = rz / rho;
   double cc = 0.0;
   const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * VT;
@@ -208,7 +264,8 @@ __global__ void __launch_bounds__(VT, 4)
         q.y = rv.y * dv.y + beta * pv.y;
         p2[k] = q;
         const int64_t node = 2 * k;
-        const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
+        uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
+        if (own) w &= (own[node >> 5] >> (node & 31)) & 3u;
         a2[k] = make_double2((w & 1u) ? q.x : 0.0, (w & 2u) ? q.y : 0.0);
         if (w & 1u) cc += q.x * q.x;
         if (w & 2u) cc += q.y * q.y;
@@ -228,10 +285,10 @@ __global__ void __launch_bounds__(VT, 4)
         const int64_t i = o + node;
         const double zi = d ? r[i] * d[i] : r[i];  // d holds 1/diag here
         const double pi = zi + beta * p[i];
-        const bool cons = is_cons(cons_mask, node);
+        const bool cw = is_cons(cons_mask, node) && owned_w(own, node) != 0.0;
         p[i] = pi;
-        Ap[i] = cons ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
-        if (cons) cc += pi * pi;
+        Ap[i] = cw ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
+        if (cw) cc += pi * pi;
       }
     }
   }
@@ -241,20 +298,27 @@ __global__ void __launch_bounds__(VT, 4)
   const double tc = pcg_sum_partials<VT>(part, gridDim.x, scratch);
   if (threadIdx.x == 0) {
     st->counter[2] = 0;
-    st->cons_pp = tc;
+    st->red[3] = tc;
+    st->it = it;
+    st->res = res;
+    hist[it] = res;
+    if (conv) st->converged = 1;
+    st->beta = beta;
+    st->rho = rz;
   }
 }
 
 // y = x on constrained rows, 0 elsewhere: the RED target of an operator apply
-// (operator.cpp:87-90,141-143).
+// (operator.cpp:87-90,141-143).  With an owner mask only the owner presets
+// (a following interface sum-exchange then leaves exactly x).
 __global__ void __launch_bounds__(VT)
     init_y_kernel(int64_t n_L, int m, const double* __restrict__ x, double* __restrict__ y,
-                  const uint32_t* cons_mask) {
+                  const uint32_t* cons_mask, const uint32_t* own) {
   const int64_t stride = (int64_t)gridDim.x * VT;
   for (int c = 0; c < m; ++c)
     for (int64_t node = (int64_t)blockIdx.x * VT + threadIdx.x; node < n_L; node += stride) {
       const int64_t i = c * n_L + node;
-      y[i] = is_cons(cons_mask, node) ? x[i] : 0.0;
+      y[i] = (is_cons(cons_mask, node) && owned_w(own, node) != 0.0) ? x[i] : 0.0;
     }
 }
 
@@ -266,39 +330,48 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr
 }  // namespace
 
 cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
-                          const uint32_t* mask) {
+                          const uint32_t* mask, const uint32_t* own) {
   if (!mask) return cudaMemsetAsync(y, 0, sizeof(double) * n_L * m, s);
-  init_y_kernel<<<vec_grid(), VT, 0, s>>>(n_L, m, x, y, mask);
+  init_y_kernel<<<vec_grid(), VT, 0, s>>>(n_L, m, x, y, mask, own);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t pcg_launch_init(cudaStream_t s, PcgState* st, int64_t n_L, int m, const double* b,
                             const double* d, double* dinv, double* x, double* r, double* p,
-                            double* Ap, const uint32_t* mask, double* part, double* hist) {
-  pcg_init_kernel<<<vec_grid(), VT, 0, s>>>(st, n_L, m, b, d, dinv, x, r, p, Ap, mask, part, hist);
+                            double* Ap, const uint32_t* mask, const uint32_t* own, double* part) {
+  pcg_init_kernel<<<vec_grid(), VT, 0, s>>>(st, n_L, m, b, d, dinv, x, r, p, Ap, mask, own, part);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n, const double* d,
-                              double* x, double* r, const double* p, const double* Ap,
-                              double* part, double* hist) {
-  if (aligned16(d) && aligned16(x) && aligned16(r) && aligned16(p) && aligned16(Ap))
-    pcg_update_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, n, d, x, r, p, Ap, part, hist);
-  else
-    pcg_update_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, n, d, x, r, p, Ap, part, hist);
+cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist) {
+  pcg_init_finalize<<<1, 32, 0, s>>>(st, hist);
   count_launch();
   return cudaGetLastError();
 }
 
-cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int64_t n_L, int m,
-                                 const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, double* part) {
+cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
+                              const double* d, double* x, double* r, const double* p,
+                              const double* Ap, const uint32_t* own, double* part) {
+  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(x) && aligned16(r) &&
+                   aligned16(p) && aligned16(Ap);
+  auto k = vec ? (own ? pcg_update_kernel<true, true> : pcg_update_kernel<true, false>)
+               : (own ? pcg_update_kernel<false, true> : pcg_update_kernel<false, false>);
+  k<<<vec_grid(), VT, 0, s>>>(st, it, n_L, m, d, x, r, p, Ap, own, part);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
+                                 int m, const double* d, const double* r, double* p, double* Ap,
+                                 const uint32_t* mask, const uint32_t* own, double* part) {
   if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
-    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, n_L, m, d, r, p, Ap, mask, part);
+    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
+                                                        own, part);
   else
-    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, n_L, m, d, r, p, Ap, mask, part);
+    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
+                                                         own, part);
   count_launch();
   return cudaGetLastError();
 }

@@ -1,4 +1,7 @@
-// Device-resident PCG state and launchers (pcg_kernels.cu).
+// Device-resident PCG launchers (pcg_kernels.cu).  d / dinv conventions:
+// the init kernel takes the Jacobi diagonal d (or nullptr) and writes
+// dinv = 1/d, which the update and direction kernels take as their `d`.
+// own: owner bitmask over scalar nodes (partitioned problems), nullptr = all.
 #pragma once
 #include "hxf_internal.h"
 
@@ -6,17 +9,16 @@ namespace hxf {
 
 int vec_grid();
 cudaError_t launch_init_y(cudaStream_t s, int64_t n_L, int m, const double* x, double* y,
-                          const uint32_t* mask);
-// d: Jacobi diagonal or nullptr; dinv receives 1/d, the operand the update
-// and direction kernels take as `d` (z = r * dinv).
+                          const uint32_t* mask, const uint32_t* own = nullptr);
 cudaError_t pcg_launch_init(cudaStream_t s, PcgState* st, int64_t n_L, int m, const double* b,
                             const double* d, double* dinv, double* x, double* r, double* p,
-                            double* Ap, const uint32_t* mask, double* part, double* hist);
-cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n, const double* d,
-                              double* x, double* r, const double* p, const double* Ap,
-                              double* part, double* hist);
-cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int64_t n_L, int m,
-                                 const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, double* part);
+                            double* Ap, const uint32_t* mask, const uint32_t* own, double* part);
+cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist);
+cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
+                              const double* d, double* x, double* r, const double* p,
+                              const double* Ap, const uint32_t* own, double* part);
+cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
+                                 int m, const double* d, const double* r, double* p, double* Ap,
+                                 const uint32_t* mask, const uint32_t* own, double* part);
 
 }  // namespace hxf
