@@ -43,7 +43,7 @@ UNIT = "GDOF/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--bp", default="bp5")
@@ -78,61 +78,94 @@ def bp_sizes(bp: str, p: int, d: int):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    NVML in-process (nvidia_ml_py) every 2 ms — the timed region of a default
+    run is only tens of ms, too short for `nvidia-smi -lms` (whose piped output
+    is also block-buffered).  Falls back to one-shot nvidia-smi queries."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reason bits)
+        self._stop = threading.Event()
+        self._nvml = None
+        self.source = None
+
+    def _open_nvml(self):
+        import pynvml as nv
+
+        nv.nvmlInit()
+        handle = None
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            handle = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            handle = nv.nvmlDeviceGetHandleByIndex(self.index)
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        mx = nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)
+
+        def sample():
+            return (nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM), mx, get_reasons(handle))
+        return sample
+
+    def _open_smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True,
+                                 text=True, timeout=5).stdout.strip().split(",")
+            return float(out[0]), float(out[1]), int(out[2].strip(), 16)
+        return sample
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._sample())
+            except Exception:
+                pass
+            self._stop.wait(0.002 if self.source == "nvml" else 0.05)
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+        for name, opener in (("nvml", self._open_nvml), ("nvidia-smi", self._open_smi)):
+            try:
+                self._sample = opener()
+                self._sample()
+                self.source = name
+                break
+            except Exception:
+                self._sample = None
+        if self._sample:
+            self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
+        if self._sample:
+            self._stop.set()
+            self.thread.join(timeout=5)
+            try:  # one more right at the end of the timed region
+                self.samples.append(self._sample())
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[2:6]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = sorted(s[0] for s in self.samples)
+        bits = 0
+        for s in self.samples:
+            bits |= int(s[2])
+        reasons = sorted(k for k, v in self.REASONS.items() if bits & v)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": self.source}
 
 
 def measured_peak():
