@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define HXF_ABI_VERSION 1
+#define HXF_ABI_VERSION 2
 
 typedef enum {
   HXF_OK = 0,
@@ -141,6 +141,10 @@ typedef struct {
   double tol_rel;       /* PcgOptions::tol_rel */
   int max_iter;         /* PcgOptions::max_iter */
   int fixed_iterations; /* PcgOptions::fixed_iterations, < 0 = unset */
+  int time_apply;       /* 1: CUDA-event time every operator apply into
+                           apply_time_seconds (the reference's timer,
+                           pcg.cpp:70-73); costs ~7 us per apply inside the
+                           fixed-iteration graph.  0: apply_time_seconds = 0 */
 } hxf_pcg_options;
 
 typedef struct {

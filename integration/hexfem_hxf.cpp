@@ -94,6 +94,7 @@ SolveReport pcg(const MatFreeOperator& op, std::span<const double> b,
   if (!jacobi_diag.empty() && int64_t(jacobi_diag.size()) != n)
     throw std::invalid_argument("pcg: preconditioner length mismatch");
   hxf_pcg_options o{};
+  o.time_apply = 1;  // SolveReport::apply_time_seconds as the reference fills it
   o.tol_rel = options.tol_rel;
   o.max_iter = options.max_iter;
   o.fixed_iterations = options.fixed_iterations ? *options.fixed_iterations : -1;

@@ -64,7 +64,8 @@ class OperatorDesc(C.Structure):
 
 
 class PcgOptions(C.Structure):
-    _fields_ = [("tol_rel", C.c_double), ("max_iter", C.c_int), ("fixed_iterations", C.c_int)]
+    _fields_ = [("tol_rel", C.c_double), ("max_iter", C.c_int), ("fixed_iterations", C.c_int),
+                ("time_apply", C.c_int)]
 
 
 class SolveReport(C.Structure):
@@ -336,13 +337,15 @@ class Operator:
         check(lib().hxf_restriction_multiplicity(self._h, out.ctypes.data, HXF_HOST))
         return out
 
-    def pcg(self, b, diag=None, tol=1e-8, max_iter=2000, fixed_iterations=None, x=None):
+    def pcg(self, b, diag=None, tol=1e-8, max_iter=2000, fixed_iterations=None, x=None,
+            time_apply=True):
         b = _f64(b)
         diag = _f64(diag)
         bp, space = _ptr(b)
         if x is None:
             x = self._out_like(b, self.size)
-        opts = PcgOptions(tol, max_iter, -1 if fixed_iterations is None else fixed_iterations)
+        opts = PcgOptions(tol, max_iter, -1 if fixed_iterations is None else fixed_iterations,
+                          int(bool(time_apply)))
         cap = (fixed_iterations if fixed_iterations is not None else max_iter) + 2
         hist = np.zeros(cap)
         rep = SolveReport(0, 0, hist.ctypes.data, cap, 0.0, 0.0)

@@ -105,6 +105,23 @@ int op_kernel_choice() {
 
 bool pencil_disabled() { return op_kernel_choice() == 2; }
 
+bool serpentine() {
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_SERPENTINE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+int dmma_warps() {
+  static const int nw = [] {
+    const char* v = std::getenv("HXF_DMMA_NW");
+    const int n = v ? std::atoi(v) : 0;
+    return (n == 2 || n == 4 || n == 8) ? n : 4;
+  }();
+  return nw;
+}
+
 int max_op_grid() { return num_sms() * 32; }
 
 cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams& prm,
@@ -139,7 +156,7 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
 // dot_part and the last CTA of the last pass derives alpha into *st.
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
                   int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr,
-                  bool halo = true) {
+                  bool halo = true, int rev = 0) {
   if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask, op->d_own), "init_y");
   OpParams prm{};
   prm.x = x;
@@ -158,6 +175,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.stop = stop;
   prm.ablate = ablate_bits();
   prm.D = op->d_G;
+  prm.rev = rev;
   const int last_pass = op->beta != 0.0 ? 1 : 0;
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
@@ -766,6 +784,7 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
 
     // (External: inside a captured graph the record is a real timing event)
     bool capturing = false;
+    const bool timed = opts->time_apply != 0;
     auto record = [&](cudaEvent_t e) {
       ck(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
                    : cudaEventRecord(e, s),
@@ -773,22 +792,27 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     };
     // one iteration: K1 (fused operator, last CTA -> alpha), update (last
     // CTA -> residual, beta, stop), direction (last CTA -> constrained p^2)
+    // serpentine sweeps: every kernel runs opposite to the one before it, so
+    // it starts on the vectors the previous kernel touched last (still in the
+    // 126 MB L2); the three-kernel cycle flips each iteration
+    const int serp = serpentine() ? 1 : 0;
     auto iteration = [&](int it) {
       int nparts = 0;
-      record(op->ev[2 * (it - 1)]);
+      const int odd = it & 1;
+      if (timed) record(op->ev[2 * (it - 1)]);
       // Ap was preset by the init / direction kernel: no memset pass here;
       // partitioned: K1 ends with the interface sum-exchange of Ap
       device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state,
-                   /*halo=*/false);
-      record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
+                   /*halo=*/false, serp & (odd ^ 1));
+      if (timed) record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
       op_halo_sum(op, Ap, s);
       op_allreduce(op, red, 1, s);  // pAp
       ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, dinv, dx, r, p, Ap, op->d_own,
-                           vpart),
+                           vpart, serp & odd),
          "pcg update");
       op_allreduce(op, red + 1, 2, s);  // r.r, r.z
       ck(pcg_launch_direction(s, op->d_state, it, hist, op->n_L, op->m, dinv, r, p, Ap,
-                              op->d_mask, op->d_own, vpart),
+                              op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
          "pcg direction");
     };
     auto init = [&] {
@@ -805,7 +829,8 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     if (fixed && op_graph_safe(op)) {
       // benchmark semantics: the whole fixed-iteration solve as one CUDA graph
       // (launch-gap free), captured once per operand set and replayed
-      const std::vector<const void*> key = {db, dd, dx, dinv, (const void*)(intptr_t)limit};
+      const std::vector<const void*> key = {db, dd, dx, dinv, (const void*)(intptr_t)limit,
+                                           (const void*)(intptr_t)timed};
       if (!op->graph_exec || op->graph_key != key) {
         if (op->graph_exec) cudaGraphExecDestroy(op->graph_exec);
         op->graph_exec = nullptr;
@@ -863,7 +888,7 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
          "history");
     }
     double apply_ms = 0;
-    for (int i = 0; i < std::min(iters, launched); ++i) {
+    for (int i = 0; timed && i < std::min(iters, launched); ++i) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, op->ev[2 * i], op->ev[2 * i + 1]), "elapsed");
       apply_ms += ms;

@@ -51,6 +51,7 @@ struct OpParams {
   int ablate;                // measurement-only ablation bits (HXF_ABLATE), 0 in production
   const double* D;           // device copy of the 1-D derivative matrix (collocated path)
   PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
+  int rev;                   // sweep elements last to first (L2 reuse across CG kernels)
 };
 
 // Is lattice node (ix, iy, iz) on a constrained face of the box (mode 1)?
@@ -96,6 +97,8 @@ int num_sms();
 // "generic" -> 2 (op_kernel.cuh only).
 int op_kernel_choice();
 bool pencil_disabled();
+bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward
+int dmma_warps();  // HXF_DMMA_NW: warps per element of op_dmma_kernel (2, 4 default, 8)
 int ablate_bits();
 void count_launch(int n = 1);
 

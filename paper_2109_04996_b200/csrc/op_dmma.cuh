@@ -8,10 +8,11 @@
 // instruction count per element ~4x; the arithmetic (and its FP64 rounding
 // model: fused multiply-adds) is unchanged.
 //
-// One element per CTA of two warps; lane l: g = l>>2, t = l&3 (the mma
-// fragment coordinates).  "dist X": a lane owns points (k, j = g, i = 2t..2t+1)
-// of the warp's planes k in {4w..4w+3}; "dist Z": (k = g, j, i = 2t..2t+1) for
-// the warp's rows j in {4w..4w+3}.
+// One element per CTA of NW warps (4 by default, KK = 8/NW planes each); lane
+// l: g = l>>2, t = l&3 (the mma fragment coordinates).  "dist X": a lane owns
+// points (k, j = g, i = 2t..2t+1) of the warp's planes k in {KK w .. KK w +
+// KK-1}; "dist Z": (k = g, j, i = 2t..2t+1) for the warp's rows j in the same
+// range.
 //   x-dir  G0_k = U_k D^T    (M = j, N = o, K = a)  -> dist X, registers
 //   y-dir  G1_k = D U_k      (M = o, N = i, K = b)  -> dist X, registers
 //   z-dir  G2_j = D U_(.j.)  (M = o, N = i, K = c)  -> dist Z -> slab Z
@@ -33,9 +34,14 @@
 
 namespace hxf {
 
-template <int NC_, int GM_>
+template <int NC_, int GM_, int NW_ = 4>
 struct DmmaTraits {
-  static constexpr int P = 8, NC = NC_, GM = GM_, P3 = 512, NT = 64;
+  // NW warps per element; warp w owns planes / rows KK w .. KK w + KK-1
+  static constexpr int P = 8, NC = NC_, GM = GM_, P3 = 512, NW = NW_, NT = 32 * NW_, KK = 8 / NW_;
+  static_assert(NW_ == 2 || NW_ == 4 || NW_ == 8, "8 planes split over NW warps");
+  // CTAs per SM the register budget is sized for (tuned at C3: NW = 4 -> 122
+  // registers, 4 CTAs; NW = 2 needs 224 registers to keep its loads in flight)
+  static constexpr int MINB = NW_ == 8 ? 3 : 4;
   static constexpr int SLAB = 512;   // doubles
   static constexpr int QDS = 6 * P3;
   static constexpr int OFF_QD = 0;
@@ -57,8 +63,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
-  constexpr int NC = T::NC, P3 = T::P3, NT = T::NT;
+__global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams prm) {
+  constexpr int NC = T::NC, P3 = T::P3, NT = T::NT, KK = T::KK;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_scratch[NT / 32 + 1];
@@ -83,9 +89,13 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
   const int64_t G = gridDim.x;
   const int64_t NXY = prm.NX * prm.NY;
   uint64_t policy = 0;
+  // sweep position -> element: last to first when prm.rev (the CG driver
+  // alternates sweep directions so each kernel starts where the previous one's
+  // most recent, L2-resident, vector traffic is)
+  auto elem = [&](int64_t e) { return prm.rev ? nsteps - 1 - e : e; };
   auto issue_qdata = [&](int64_t e) {
     mbar_arrive_expect_tx(&qbar, (uint32_t)(T::QDS * 8));
-    bulk_g2s(sQD, prm.qd + e * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);
+    bulk_g2s(sQD, prm.qd + elem(e) * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);
   };
   if (tid == 0) {
     mbar_init(&qbar, 1);
@@ -104,22 +114,23 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
   auto node_of = [&](const Geo& q, int kk, int h) -> int64_t {
     if constexpr (T::GM == 0) return q.key + (int64_t)kk * NXY + h;
     if (prm.idx)
-      return (int64_t)prm.idx[q.key * P3 + (2 * t + h) + 8 * (g + 8 * (4 * w + kk))];
+      return (int64_t)prm.idx[q.key * P3 + (2 * t + h) + 8 * (g + 8 * (KK * w + kk))];
     return q.key + (int64_t)kk * NXY + h;
   };
-  auto geometry = [&](int64_t e) {
+  auto geometry = [&](int64_t s) {
     Geo q{};
-    q.active = e < nsteps;
+    q.active = s < nsteps;
     if (!q.active) return q;
+    const int64_t e = elem(s);
     if (T::GM == 1 && prm.idx) {
       q.key = e;
     } else {
       const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      const int64_t ix = ex * 7 + 2 * t, iy = ey * 7 + g, iz = ez * 7 + 4 * w;
+      const int64_t ix = ex * 7 + 2 * t, iy = ey * 7 + g, iz = ez * 7 + KK * w;
       q.key = ix + prm.NX * iy + NXY * iz;
       if (T::GM == 0 && prm.cons_mode == 1) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (on_bnd_face(prm, ix + h, iy, iz + kk)) q.cmask |= 1u << (2 * kk + h);
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
     }
     if (T::GM == 1 && prm.cons_mode == 2) {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
+      for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t node = node_of(q, kk, h);
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
                                                          8 * q.key) & 15u) == 0 &&
         (prm.NX & 1) == 0) {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < KK; ++kk) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(xc + node_of(q, kk, 0)));
         xn[2 * kk] = v.x;
         xn[2 * kk + 1] = v.y;
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
       return;
     }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
+    for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         xn[2 * kk + h] = (q.active && !(prm.ablate & 1)) ? __ldg(xc + node_of(q, kk, h)) : 1.0;
@@ -161,11 +172,11 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
 
   Geo gcur = geometry(blockIdx.x);
   Geo gpf = NC > 1 ? gcur : geometry(blockIdx.x + G);
-  double xn[8];
+  double xn[2 * KK];
   load_lines(gcur, 0, xn);
-  double u[8];
+  double u[2 * KK];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
+  for (int m = 0; m < 2 * KK; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
   load_lines(gpf, 1 % NC, xn);
   __syncthreads();  // mbarrier init visible
 
@@ -178,31 +189,31 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
       double* yc = prm.y + c * prm.n_L;
       // ---- G: this lane's masked dist-X pairs into slab A ----
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        *reinterpret_cast<double2*>(SA + T::off(4 * w + kk, g, 2 * t)) =
+      for (int kk = 0; kk < KK; ++kk)
+        *reinterpret_cast<double2*>(SA + T::off(KK * w + kk, g, 2 * t)) =
             make_double2(u[2 * kk], u[2 * kk + 1]);
       // next item's raw lines: land while this item computes
       {
         const Geo gnext = ((q + 2) / NC == (q + 1) / NC && NC > 1)
                               ? gpf
                               : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
-        double nx_[8];
+        double nx_[2 * KK];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) nx_[m] = xn[m];
+        for (int m = 0; m < 2 * KK; ++m) nx_[m] = xn[m];
         // masked values of item q+1 are formed when it starts (gpf)
         load_lines(gnext, (q + 2) % NC, xn);
 #pragma unroll
-        for (int m = 0; m < 8; ++m)
+        for (int m = 0; m < 2 * KK; ++m)
           u[m] = (gpf.active && !((gpf.cmask >> m) & 1u)) ? nx_[m] : 0.0;  // item q+1
         gpf = gnext;
       }
       __syncthreads();  // (A) slab A complete
 
       // ---- forward contractions ----
-      double g0[4][2], g1[4][2];
+      double g0[KK][2], g1[KK][2];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * w + kk;
+      for (int kk = 0; kk < KK; ++kk) {
+        const int k = KK * w + kk;
         double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
@@ -215,8 +226,8 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
         g1[kk][1] = d1;
       }
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = 4 * w + jj;
+      for (int jj = 0; jj < KK; ++jj) {
+        const int j = KK * w + jj;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dr[ks], SA[T::off(4 * ks + t, j, g)]);
@@ -228,8 +239,8 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
       // ---- QFunction on dist X (qfunction.cpp:135-162) ----
       double energy = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * w + kk;
+      for (int kk = 0; kk < KK; ++kk) {
+        const int k = KK * w + kk;
         const int sp = T::off(k, g, 2 * t);
         const double2 z2 = *reinterpret_cast<const double2*>(SZ + sp);
         const int pt = k * 64 + g * 8 + 2 * t;
@@ -260,10 +271,10 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
       if (c == NC - 1 && tid == 0 && e + G < nsteps && !(prm.ablate & 4)) issue_qdata(e + G);
 
       // ---- transposed contractions ----
-      double y01[4][2];
+      double y01[KK][2];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * w + kk;
+      for (int kk = 0; kk < KK; ++kk) {
+        const int k = KK * w + kk;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
@@ -273,10 +284,10 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
         y01[kk][0] = c0;
         y01[kk][1] = c1;
       }
-      double y2z[4][2];
+      double y2z[KK][2];
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = 4 * w + jj;
+      for (int jj = 0; jj < KK; ++jj) {
+        const int j = KK * w + jj;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dc[ks], SZ[T::off(4 * ks + t, j, g)]);  // z^T
@@ -285,16 +296,16 @@ __global__ void __launch_bounds__(T::NT) op_dmma_kernel(const OpParams prm) {
       }
       __syncthreads();  // (D) slab B (V1) free
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-        *reinterpret_cast<double2*>(SB + T::off(g, 4 * w + jj, 2 * t)) =
+      for (int jj = 0; jj < KK; ++jj)
+        *reinterpret_cast<double2*>(SB + T::off(g, KK * w + jj, 2 * t)) =
             make_double2(y2z[jj][0], y2z[jj][1]);
       __syncthreads();  // (E) Y2 in slab B (dist Z)
 
       // ---- combine on dist X, G^T scatter (constrained rows preset by the caller) ----
       if (gcur.active) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const double2 z2 = *reinterpret_cast<const double2*>(SB + T::off(4 * w + kk, g, 2 * t));
+        for (int kk = 0; kk < KK; ++kk) {
+          const double2 z2 = *reinterpret_cast<const double2*>(SB + T::off(KK * w + kk, g, 2 * t));
           const double yk0 = prm.coef * (y01[kk][0] + z2.x);
           const double yk1 = prm.coef * (y01[kk][1] + z2.y);
           if (!(prm.ablate & 2)) {

@@ -97,10 +97,22 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   return cudaGetLastError();
 }
 
+template <int NC, int NW>
+cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
+  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW>>(prm, s, g);
+  return run_dmma<DmmaTraits<NC, 1, NW>>(prm, s, g);
+}
+
 template <int NC>
 cudaError_t run_dmma_gm(const OpParams& prm, cudaStream_t s, int* g) {
-  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0>>(prm, s, g);
-  return run_dmma<DmmaTraits<NC, 1>>(prm, s, g);
+  switch (dmma_warps()) {
+    case 8:
+      return run_dmma_nw<NC, 8>(prm, s, g);
+    case 2:
+      return run_dmma_nw<NC, 2>(prm, s, g);
+    default:
+      return run_dmma_nw<NC, 4>(prm, s, g);
+  }
 }
 
 template <int P, int NC>

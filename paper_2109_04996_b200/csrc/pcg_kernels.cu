@@ -125,7 +125,7 @@ template <bool VEC, bool OWN>
 __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
     pcg_update_kernel(PcgState* st, int it, int64_t n_L, int m, const double* __restrict__ d,
                       double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                      const double* __restrict__ Ap, const uint32_t* own, double* part) {
+                      const double* __restrict__ Ap, const uint32_t* own, double* part, int rev) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
   const double pap = st->red[0];
@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
       const double2* d2 = reinterpret_cast<const double2*>(d + o);
       const double2 one2 = make_double2(1.0, 1.0);
       auto two = [&](int64_t k, double2 xv, double2 pv, double2 rv, double2 av, double2 dv) {
+        // (k is already the swept pair index)
         xv.x += alpha * pv.x;
         xv.y += alpha * pv.y;
         rv.x -= alpha * av.x;
@@ -176,17 +177,21 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
           rz += rv.x * (rv.x * dv.x) + rv.y * (rv.y * dv.y);
         }
       };
-      int64_t k = tid;
-      for (; k + stride < h; k += 2 * stride) {
-        const int64_t k1 = k + stride;
+      int64_t j = tid;
+      for (; j + stride < h; j += 2 * stride) {
+        const int64_t k = rev ? h - 1 - j : j, k1 = rev ? k - stride : k + stride;
         const double2 xa = x2[k], pa = p2[k], ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
         const double2 xb = x2[k1], pb = p2[k1], rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
         two(k, xa, pa, ra, aa, da);
         two(k1, xb, pb, rb, ab, db);
       }
-      if (k < h) two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
+      if (j < h) {
+        const int64_t k = rev ? h - 1 - j : j;
+        two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
+      }
     } else {
-      for (int64_t node = tid; node < n_L; node += stride) {
+      for (int64_t jn = tid; jn < n_L; jn += stride) {
+        const int64_t node = rev ? n_L - 1 - jn : jn;
         const int64_t i = o + node;
         x[i] += alpha * p[i];
         const double ri = r[i] - alpha * Ap[i];
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(VT, 4)
     pcg_direction_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                          const double* __restrict__ d, const double* __restrict__ r,
                          double* __restrict__ p, double* __restrict__ Ap,
-                         const uint32_t* cons_mask, const uint32_t* own, double* part) {
+                         const uint32_t* cons_mask, const uint32_t* own, double* part, int rev) {
   __shared__ double scratch[VT / 32];
   if (st->stop) return;
   const double rr = st->red[1], rz = st->red[2];
@@ -271,17 +276,21 @@ __global__ void __launch_bounds__(VT, 4)
         if (w & 2u) cc += q.y * q.y;
       };
       const double2 one2 = make_double2(1.0, 1.0);
-      int64_t k = tid;
-      for (; k + stride < h; k += 2 * stride) {
-        const int64_t k1 = k + stride;
+      int64_t j = tid;
+      for (; j + stride < h; j += 2 * stride) {
+        const int64_t k = rev ? h - 1 - j : j, k1 = rev ? k - stride : k + stride;
         const double2 ra = r2[k], pa = p2[k], da = d ? d2[k] : one2;
         const double2 rb = r2[k1], pb = p2[k1], db = d ? d2[k1] : one2;
         two(k, ra, pa, da);
         two(k1, rb, pb, db);
       }
-      if (k < h) two(k, r2[k], p2[k], d ? d2[k] : one2);
+      if (j < h) {
+        const int64_t k = rev ? h - 1 - j : j;
+        two(k, r2[k], p2[k], d ? d2[k] : one2);
+      }
     } else {
-      for (int64_t node = tid; node < n_L; node += stride) {
+      for (int64_t jn = tid; jn < n_L; jn += stride) {
+        const int64_t node = rev ? n_L - 1 - jn : jn;
         const int64_t i = o + node;
         const double zi = d ? r[i] * d[i] : r[i];  // d holds 1/diag here
         const double pi = zi + beta * p[i];
@@ -353,25 +362,25 @@ cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist)
 
 cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
                               const double* d, double* x, double* r, const double* p,
-                              const double* Ap, const uint32_t* own, double* part) {
+                              const double* Ap, const uint32_t* own, double* part, int rev) {
   const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(x) && aligned16(r) &&
                    aligned16(p) && aligned16(Ap);
   auto k = vec ? (own ? pcg_update_kernel<true, true> : pcg_update_kernel<true, false>)
                : (own ? pcg_update_kernel<false, true> : pcg_update_kernel<false, false>);
-  k<<<vec_grid(), VT, 0, s>>>(st, it, n_L, m, d, x, r, p, Ap, own, part);
+  k<<<vec_grid(), VT, 0, s>>>(st, it, n_L, m, d, x, r, p, Ap, own, part, rev);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
                                  int m, const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, const uint32_t* own, double* part) {
+                                 const uint32_t* mask, const uint32_t* own, double* part, int rev) {
   if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
     pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
-                                                        own, part);
+                                                        own, part, rev);
   else
     pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
-                                                         own, part);
+                                                         own, part, rev);
   count_launch();
   return cudaGetLastError();
 }

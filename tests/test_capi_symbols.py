@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_error_channel():
     lib = capi.lib()
-    assert lib.hxf_abi_version() == 1
+    assert lib.hxf_abi_version() == 2
     assert isinstance(lib.hxf_last_error(), bytes)
 
 
