@@ -11,7 +11,9 @@ per step (the reference's bench mode, proj/src/bench.cpp:191-229).
            384 MB > 126 MB L2, so no L2 flush is needed between steps)
   apply    GDOF/s of a single operator apply y = A x (memset + fused kernel)
   e2e      the same CG step through the public API with HOST (pinned)
-           b in / x out: H2D + solve + D2H inside the timed region
+           b in / x out: every step's H2D(b) + solve + D2H(x) inside the
+           timed region, consecutive steps pipelined (copies of neighbouring
+           solves overlap the current solve; Problem.pcg_host_batch)
   roofline the fused operator kernel: algorithmic bytes per launch
            (16 m n_L + 48 E q^3) / its event-timed duration,
            against MEASURED_PEAKS.json hbm_gbs
@@ -345,22 +347,24 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_apply = a0.elapsed_time(a1) * 1e-3 / reps
 
-    # e2e: pinned host b in, host x out, through the public API
-    b_host = torch.from_numpy(prob.rhs).pin_memory()
-    x_host = torch.empty(n_vec, dtype=torch.float64).pin_memory()
-    prob.pcg_host(b_host.data_ptr(), x_host.data_ptr(), fixed_iterations=args.iters,
-                  time_apply=False)
+    # e2e: pinned host b in, host x out, through the public API: consecutive
+    # solves, each with its own H2D(b) and D2H(x), the copies of neighbouring
+    # solves overlapped with the current one (Problem.pcg_host_batch)
+    b_host = [torch.from_numpy(prob.rhs).pin_memory() for _ in range(2)]
+    x_host = [torch.empty(n_vec, dtype=torch.float64).pin_memory() for _ in range(2)]
+    bs = [b_host[k % 2].data_ptr() for k in range(args.steps)]
+    xs = [x_host[k % 2].data_ptr() for k in range(args.steps)]
+    prob.pcg_host_batch(bs[:2], xs[:2], fixed_iterations=args.iters)  # warm (graphs)
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record(stream)
-    for _ in range(args.steps):
-        prob.pcg_host(b_host.data_ptr(), x_host.data_ptr(), fixed_iterations=args.iters,
-                      time_apply=False)
+    reps = prob.pcg_host_batch(bs, xs, fixed_iterations=args.iters)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3) / args.steps
+    assert all(r["iterations"] == args.iters for r in reps)
     if world > 1:
         t = torch.tensor([e2e_ms, t_apply], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

@@ -159,6 +159,15 @@ typedef struct {
 int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_options* opts,
             double* x, hxf_memspace space, hxf_solve_report* report);
 
+/* nrhs consecutive solves with the same operator from HOST vectors b[k] into
+ * x[k] (pinned memory for overlap), diag on the DEVICE (or NULL).  Pipelined
+ * over three engines: the copy-in of b[k+1] and the copy-out of x[k-1] run
+ * while solve k computes; each solve is exactly hxf_pcg's.  time_apply is
+ * ignored (no per-apply events); reports[k].total_time_seconds is the batch's
+ * device time / nrhs. */
+int hxf_pcg_host_batch(hxf_op* op, int nrhs, const double* const* b, const double* diag,
+                       const hxf_pcg_options* opts, double* const* x, hxf_solve_report* reports);
+
 /* ---- partitioned box (multi-GPU) ---------------------------
  * The reference has no distributed layer (shared-memory threads only,
  * proj/src/parallel.cpp); this is the B200 extension its paper describes as

@@ -29,7 +29,7 @@ EXPORTS = (
     "hxf_comm_unique_id", "hxf_comm_create_nccl", "hxf_comm_wrap_nccl", "hxf_comm_group_create",
     "hxf_comm_group_destroy", "hxf_comm_create_group", "hxf_comm_destroy", "hxf_comm_rank",
     "hxf_comm_size", "hxf_comm_allreduce_sum", "hxf_operator_set_partition",
-    "hxf_operator_halo_sum",
+    "hxf_operator_halo_sum", "hxf_pcg_host_batch",
 )
 
 
@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
     L.hxf_comm_allreduce_sum.argtypes = [P, P, I64, P]
     L.hxf_operator_set_partition.argtypes = [P, P, C.POINTER(PartitionDesc)]
     L.hxf_operator_halo_sum.argtypes = [P, P, I]
+    L.hxf_pcg_host_batch.argtypes = [P, I, P, P, C.POINTER(PcgOptions), P, P]
     _lib = L
     return L
 

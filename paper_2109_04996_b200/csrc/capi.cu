@@ -105,6 +105,14 @@ int op_kernel_choice() {
 
 bool pencil_disabled() { return op_kernel_choice() == 2; }
 
+bool pdl_enabled() {  // measured neutral in the CG graph at C3: opt-in
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_PDL");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 bool serpentine() {
   static const bool on = [] {
     const char* v = std::getenv("HXF_SERPENTINE");
@@ -267,9 +275,190 @@ void upload_qdata(hxf_op* op, const double* src, int nplanes, hxf_memspace space
      "qdata upload");
 }
 
+
+// ---------------------------------------------------------------- PCG driver
+// One device-resident Jacobi-PCG solve (pcg.cpp:24-115) on op's stream:
+// init (x = 0, r = b, p = z, dinv = 1/diag, ||b||, rho) then per iteration
+//   K1 (Ap += A p, last CTA: pAp) -> [halo sum Ap, all-reduce pAp]
+//   update (alpha; x, r; r.r, r.z) -> [all-reduce] -> direction (beta; p, Ap preset)
+struct PcgSolve {
+  hxf_op* op;
+  const double* db;
+  const double* dd;
+  double* dx;
+  double* dinv;
+  int limit;
+  bool fixed, timed;
+};
+
+double* state_red(hxf_op* op) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(op->d_state) +
+                                   offsetof(PcgState, red));
+}
+
+void pcg_prepare(hxf_op* op, int limit) {
+  if (!op->d_state) op->d_state = dalloc<PcgState>(2);  // [0] live, [1] per-call template
+  if (!op->ev_t0) {
+    ck(cudaEventCreate(&op->ev_t0), "event");
+    ck(cudaEventCreate(&op->ev_t1), "event");
+  }
+  while (op->ev.size() < size_t(2 * limit)) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    op->ev.push_back(e);
+  }
+  const size_t n = size_t(op->size());
+  op->w_r.ensure(n);
+  op->w_p.ensure(n);
+  op->w_Ap.ensure(n);
+  op->w_vpart.ensure(size_t(3 * vec_grid()));  // per-CTA partials (<= 3 per CTA)
+  op->w_hist.ensure(size_t(limit) + 2);
+}
+
+// the solve's kernels (captured into a graph or run eagerly)
+void pcg_enqueue_init(const PcgSolve& ps, cudaStream_t s) {
+  hxf_op* op = ps.op;
+  ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, ps.db, ps.dd, ps.dinv, ps.dx, op->w_r.p,
+                     op->w_p.p, op->w_Ap.p, op->d_mask, op->d_own, op->w_vpart.p),
+     "pcg init");
+  op_allreduce(op, state_red(op) + 4, 2, s);  // b.b, b.z
+  ck(pcg_launch_init_finalize(s, op->d_state, op->w_hist.p), "pcg init");
+}
+
+void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capturing) {
+  hxf_op* op = ps.op;
+  double *r = op->w_r.p, *p = op->w_p.p, *Ap = op->w_Ap.p, *vpart = op->w_vpart.p;
+  double* red = state_red(op);
+  auto record = [&](cudaEvent_t e) {
+    // (External: inside a captured graph the record is a real timing event)
+    ck(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s),
+       "event");
+  };
+  // serpentine sweeps: every kernel runs opposite to the one before it, so it
+  // starts on the vectors the previous kernel touched last (still in the
+  // 126 MB L2); the three-kernel cycle flips each iteration
+  const int serp = serpentine() ? 1 : 0, odd = it & 1;
+  int nparts = 0;
+  if (ps.timed) record(op->ev[2 * (it - 1)]);
+  // Ap was preset by the init / direction kernel: no memset pass here
+  device_apply(op, p, Ap, s, op->d_part, &nparts, &op->d_state->stop, /*zero_y=*/false,
+               op->d_state, /*halo=*/false, serp & (odd ^ 1));
+  if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
+  op_halo_sum(op, Ap, s);                          // partitioned: assemble interface rows
+  op_allreduce(op, red, 1, s);                     // pAp
+  ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, ps.dinv, ps.dx, r, p, Ap, op->d_own,
+                       vpart, serp & odd),
+     "pcg update");
+  op_allreduce(op, red + 1, 2, s);  // r.r, r.z
+  ck(pcg_launch_direction(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, p, Ap,
+                          op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
+     "pcg direction");
+}
+
+// fixed-iteration solve as one CUDA graph (launch-gap free), captured once per
+// operand set and replayed; a small per-operator cache serves alternating
+// operand sets (pipelined batches)
+void pcg_launch_fixed_graph(const PcgSolve& ps, cudaStream_t s) {
+  hxf_op* op = ps.op;
+  const std::vector<const void*> key = {ps.db, ps.dd, ps.dx, ps.dinv,
+                                        (const void*)(intptr_t)ps.limit,
+                                        (const void*)(intptr_t)ps.timed, (const void*)s};
+  hxf_op::Graph* g = nullptr;
+  for (auto& cand : op->graphs)
+    if (cand.key == key) g = &cand;
+  if (!g) {
+    if (op->graphs.size() >= 4) {
+      cudaGraphExecDestroy(op->graphs.front().exec);
+      op->graphs.erase(op->graphs.begin());
+    }
+    hxf_op::Graph ng;
+    ng.key = key;
+    const int64_t before = hxf_launch_count();
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "capture");
+    pcg_enqueue_init(ps, s);
+    for (int it = 1; it <= ps.limit; ++it) pcg_enqueue_iteration(ps, it, s, true);
+    ck(cudaStreamEndCapture(s, &graph), "capture");
+    const cudaError_t ierr = cudaGraphInstantiate(&ng.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    ck(ierr, "graph instantiate");
+    ng.kernels = hxf_launch_count() - before;
+    count_launch(-int(ng.kernels));  // counted on replay below
+    op->graphs.push_back(ng);
+    g = &op->graphs.back();
+  }
+  ck(cudaGraphLaunch(g->exec, s), "graph launch");
+  count_launch(int(g->kernels));
+}
+
+// Enqueue a whole solve; tolerance mode polls the stop flag every few
+// iterations (host sync), fixed mode never syncs.  Returns iterations launched.
+int pcg_enqueue_solve(const PcgSolve& ps, cudaStream_t s) {
+  hxf_op* op = ps.op;
+  // per-call template state (uploaded by the caller) -> live state
+  ck(cudaMemcpyAsync(op->d_state, op->d_state + 1, sizeof(PcgState), cudaMemcpyDeviceToDevice, s),
+     "state");
+  if (ps.fixed && op_graph_safe(op)) {
+    pcg_launch_fixed_graph(ps, s);
+    return ps.limit;
+  }
+  pcg_enqueue_init(ps, s);
+  if (ps.fixed) {  // host-synchronous communicator: no graph capture
+    for (int it = 1; it <= ps.limit; ++it) pcg_enqueue_iteration(ps, it, s, false);
+    return ps.limit;
+  }
+  int launched = 0;
+  PcgState hs{};
+  ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
+  ck(cudaStreamSynchronize(s), "pcg init");
+  while (!hs.stop && launched < ps.limit) {
+    const int chunk = std::min(ps.limit - launched, launched < 4 ? 1 : 8);
+    for (int i = 0; i < chunk; ++i) pcg_enqueue_iteration(ps, ++launched, s, false);
+    ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
+    ck(cudaStreamSynchronize(s), "pcg");
+  }
+  return launched;
+}
+
+void pcg_upload_template(hxf_op* op, const hxf_pcg_options* opts, int limit, bool fixed,
+                         cudaStream_t s) {
+  PcgState st{};
+  st.tol = opts->tol_rel;
+  st.limit = limit;
+  st.fixed = fixed ? 1 : 0;
+  h2d(op->d_state + 1, &st, sizeof st, s);
+}
+
+void pcg_fill_report(hxf_op* op, const PcgState& hs, const double* hist_dev, int launched,
+                     bool timed, hxf_solve_report* report) {
+  if (hs.error) {
+    static const char* msgs[] = {"", "pcg: right-hand side is not finite",
+                                 "pcg: NaN in operator apply",
+                                 "pcg: indefinite direction (p^T A p <= 0), operator is not SPD",
+                                 "pcg: residual is not finite"};
+    fail(HXF_ENUMERIC, msgs[hs.error]);
+  }
+  const int iters = hs.it;
+  report->iterations = iters;
+  report->converged = (hs.converged || hs.res <= hs.target) ? 1 : 0;
+  if (report->residual_history && report->history_capacity > 0) {
+    const int nh = std::min(report->history_capacity, iters + 1);
+    ck(cudaMemcpy(report->residual_history, hist_dev, size_t(nh) * 8, cudaMemcpyDeviceToHost),
+       "history");
+  }
+  double apply_ms = 0;
+  for (int i = 0; timed && i < std::min(iters, launched); ++i) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, op->ev[2 * i], op->ev[2 * i + 1]), "elapsed");
+    apply_ms += ms;
+  }
+  report->apply_time_seconds = apply_ms * 1e-3;
+}
+
 }  // namespace
 
 extern "C" {
+
 
 const char* hxf_last_error(void) { return g_err.c_str(); }
 int hxf_abi_version(void) { return HXF_ABI_VERSION; }
@@ -743,160 +932,102 @@ int hxf_pcg(hxf_op* op, const double* b, const double* diag, const hxf_pcg_optio
     const bool fixed = opts->fixed_iterations >= 0;
     const int limit = fixed ? opts->fixed_iterations : opts->max_iter;
     if (limit < 0) fail(HXF_EINVAL, "pcg: negative iteration limit");
-    if (!op->d_state) op->d_state = dalloc<PcgState>(1);
-    if (!op->ev_t0) {
-      ck(cudaEventCreate(&op->ev_t0), "event");
-      ck(cudaEventCreate(&op->ev_t1), "event");
-    }
-    while (op->ev.size() < size_t(2 * limit)) {
-      cudaEvent_t e;
-      ck(cudaEventCreate(&e), "event");
-      op->ev.push_back(e);
-    }
-    // operands
-    const double *db = b, *dd = diag;
-    double* dx = x;
+    pcg_prepare(op, limit);
+    PcgSolve ps{op, b, diag, x, nullptr, limit, fixed, opts->time_apply != 0};
     if (space == HXF_HOST) {
       double* tb = op->w_b.ensure(n);
       h2d(tb, b, n * 8, s);
-      db = tb;
+      ps.db = tb;
       if (diag) {
         double* td = op->w_d.ensure(n);
         h2d(td, diag, n * 8, s);
-        dd = td;
+        ps.dd = td;
       }
-      dx = op->w_x.ensure(n);
+      ps.dx = op->w_x.ensure(n);
     }
-    double* r = op->w_r.ensure(n);
-    double* p = op->w_p.ensure(n);
-    double* Ap = op->w_Ap.ensure(n);
-    double* dinv = dd ? op->w_dinv.ensure(n) : nullptr;  // 1/diag, filled by the init kernel
-    const int vg = vec_grid();
-    double* vpart = op->w_vpart.ensure(size_t(3 * vg));  // per-CTA partials (<= 3 per CTA)
-    double* hist = op->w_hist.ensure(size_t(limit) + 2);
-    PcgState st{};
-    st.tol = opts->tol_rel;
-    st.limit = limit;
-    st.fixed = fixed ? 1 : 0;
-    const int* stop = &op->d_state->stop;
-    double* red = reinterpret_cast<double*>(reinterpret_cast<char*>(op->d_state) +
-                                            offsetof(PcgState, red));  // device slots
-
-    // (External: inside a captured graph the record is a real timing event)
-    bool capturing = false;
-    const bool timed = opts->time_apply != 0;
-    auto record = [&](cudaEvent_t e) {
-      ck(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
-                   : cudaEventRecord(e, s),
-         "event");
-    };
-    // one iteration: K1 (fused operator, last CTA -> alpha), update (last
-    // CTA -> residual, beta, stop), direction (last CTA -> constrained p^2)
-    // serpentine sweeps: every kernel runs opposite to the one before it, so
-    // it starts on the vectors the previous kernel touched last (still in the
-    // 126 MB L2); the three-kernel cycle flips each iteration
-    const int serp = serpentine() ? 1 : 0;
-    auto iteration = [&](int it) {
-      int nparts = 0;
-      const int odd = it & 1;
-      if (timed) record(op->ev[2 * (it - 1)]);
-      // Ap was preset by the init / direction kernel: no memset pass here;
-      // partitioned: K1 ends with the interface sum-exchange of Ap
-      device_apply(op, p, Ap, s, op->d_part, &nparts, stop, /*zero_y=*/false, op->d_state,
-                   /*halo=*/false, serp & (odd ^ 1));
-      if (timed) record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
-      op_halo_sum(op, Ap, s);
-      op_allreduce(op, red, 1, s);  // pAp
-      ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, dinv, dx, r, p, Ap, op->d_own,
-                           vpart, serp & odd),
-         "pcg update");
-      op_allreduce(op, red + 1, 2, s);  // r.r, r.z
-      ck(pcg_launch_direction(s, op->d_state, it, hist, op->n_L, op->m, dinv, r, p, Ap,
-                              op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
-         "pcg direction");
-    };
-    auto init = [&] {
-      ck(pcg_launch_init(s, op->d_state, op->n_L, op->m, db, dd, dinv, dx, r, p, Ap, op->d_mask,
-                         op->d_own, vpart),
-         "pcg init");
-      op_allreduce(op, red + 4, 2, s);  // b.b, b.z
-      ck(pcg_launch_init_finalize(s, op->d_state, hist), "pcg init");
-    };
-
-    int launched = 0;
+    ps.dinv = ps.dd ? op->w_dinv.ensure(n) : nullptr;  // 1/diag, filled by the init kernel
     ck(cudaEventRecord(op->ev_t0, s), "event");
-    h2d(op->d_state, &st, sizeof st, s);
-    if (fixed && op_graph_safe(op)) {
-      // benchmark semantics: the whole fixed-iteration solve as one CUDA graph
-      // (launch-gap free), captured once per operand set and replayed
-      const std::vector<const void*> key = {db, dd, dx, dinv, (const void*)(intptr_t)limit,
-                                           (const void*)(intptr_t)timed};
-      if (!op->graph_exec || op->graph_key != key) {
-        if (op->graph_exec) cudaGraphExecDestroy(op->graph_exec);
-        op->graph_exec = nullptr;
-        const int64_t before = hxf_launch_count();
-        cudaGraph_t graph;
-        ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed), "capture");
-        capturing = true;
-        init();
-        for (int it = 1; it <= limit; ++it) iteration(it);
-        capturing = false;
-        ck(cudaStreamEndCapture(s, &graph), "capture");
-        ck(cudaGraphInstantiate(&op->graph_exec, graph, 0), "graph instantiate");
-        cudaGraphDestroy(graph);
-        op->graph_key = key;
-        op->graph_kernels = hxf_launch_count() - before;
-        count_launch(-int(op->graph_kernels));  // counted on replay below
-      }
-      ck(cudaGraphLaunch(op->graph_exec, s), "graph launch");
-      count_launch(int(op->graph_kernels));
-      launched = limit;
-    } else if (fixed) {  // host-synchronous communicator: no graph capture
-      init();
-      for (int it = 1; it <= limit; ++it) iteration(it);
-      launched = limit;
-    } else {
-      init();
-      PcgState hs{};
-      ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
-      ck(cudaStreamSynchronize(s), "pcg init");
-      while (!hs.stop && launched < limit) {
-        const int chunk = std::min(limit - launched, launched < 4 ? 1 : 8);
-        for (int i = 0; i < chunk; ++i) iteration(++launched);
-        ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
-        ck(cudaStreamSynchronize(s), "pcg");
-      }
-    }
+    pcg_upload_template(op, opts, limit, fixed, s);
+    const int launched = pcg_enqueue_solve(ps, s);
     ck(cudaEventRecord(op->ev_t1, s), "event");
     PcgState hs{};
     ck(cudaMemcpyAsync(&hs, op->d_state, sizeof hs, cudaMemcpyDeviceToHost, s), "state");
-    if (space == HXF_HOST) d2h(x, dx, n * 8, s);
+    if (space == HXF_HOST) d2h(x, ps.dx, n * 8, s);
     ck(cudaStreamSynchronize(s), "pcg");
-    if (hs.error) {
-      static const char* msgs[] = {"", "pcg: right-hand side is not finite",
-                                   "pcg: NaN in operator apply",
-                                   "pcg: indefinite direction (p^T A p <= 0), operator is not SPD",
-                                   "pcg: residual is not finite"};
-      fail(HXF_ENUMERIC, msgs[hs.error]);
-    }
-    const int iters = hs.it;
-    report->iterations = iters;
-    report->converged = (hs.converged || hs.res <= hs.target) ? 1 : 0;
-    if (report->residual_history && report->history_capacity > 0) {
-      const int nh = std::min(report->history_capacity, iters + 1);
-      ck(cudaMemcpy(report->residual_history, hist, size_t(nh) * 8, cudaMemcpyDeviceToHost),
-         "history");
-    }
-    double apply_ms = 0;
-    for (int i = 0; timed && i < std::min(iters, launched); ++i) {
-      float ms = 0;
-      ck(cudaEventElapsedTime(&ms, op->ev[2 * i], op->ev[2 * i + 1]), "elapsed");
-      apply_ms += ms;
-    }
+    pcg_fill_report(op, hs, op->w_hist.p, launched, ps.timed, report);
     float tot = 0;
     ck(cudaEventElapsedTime(&tot, op->ev_t0, op->ev_t1), "elapsed");
-    report->apply_time_seconds = apply_ms * 1e-3;
     report->total_time_seconds = tot * 1e-3;
+  });
+}
+
+int hxf_pcg_host_batch(hxf_op* op, int nrhs, const double* const* b, const double* diag,
+                       const hxf_pcg_options* opts, double* const* x, hxf_solve_report* reports) {
+  return guarded([&] {
+    if (!op || nrhs < 0 || (nrhs > 0 && (!b || !x || !reports)) || !opts)
+      fail(HXF_EINVAL, "pcg_host_batch: NULL argument");
+    if (nrhs == 0) return;
+    cudaStream_t s = op->ctx->stream;
+    const size_t n = size_t(op->size());
+    const bool fixed = opts->fixed_iterations >= 0;
+    const int limit = fixed ? opts->fixed_iterations : opts->max_iter;
+    if (limit < 0) fail(HXF_EINVAL, "pcg: negative iteration limit");
+    pcg_prepare(op, limit);
+    if (!op->s_h2d) {
+      ck(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking), "stream");
+      for (int k = 0; k < 2; ++k)
+        for (cudaEvent_t* e : {&op->ev_b[k], &op->ev_solved[k], &op->ev_x[k]})
+          ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    }
+    double* dinv = diag ? op->w_dinv.ensure(n) : nullptr;
+    double* db[2] = {op->w_b.ensure(n), op->w_b2.ensure(n)};
+    double* dx[2] = {op->w_x.ensure(n), op->w_x2.ensure(n)};
+    // per-solve state + history snapshots, read back once at the end
+    const size_t hstride = size_t(limit) + 2;
+    double* states = op->w_states.ensure(size_t(nrhs) * (sizeof(PcgState) / 8 + 1) + 1);
+    double* hists = op->w_hists.ensure(size_t(nrhs) * hstride);
+    const size_t sst = sizeof(PcgState) / 8 + 1;
+    ck(cudaEventRecord(op->ev_t0, s), "event");
+    pcg_upload_template(op, opts, limit, fixed, s);
+    std::vector<int> launched(static_cast<size_t>(nrhs), 0);
+    // three engines: H2D of b(k+1) and D2H of x(k-1) run under solve k
+    for (int k = 0; k < nrhs; ++k) {
+      const int sl = k & 1;
+      if (k >= 2) ck(cudaStreamWaitEvent(op->s_h2d, op->ev_solved[sl], 0), "wait");
+      ck(cudaMemcpyAsync(db[sl], b[k], n * 8, cudaMemcpyHostToDevice, op->s_h2d), "H2D b");
+      ck(cudaEventRecord(op->ev_b[sl], op->s_h2d), "event");
+      ck(cudaStreamWaitEvent(s, op->ev_b[sl], 0), "wait");
+      if (k >= 2) ck(cudaStreamWaitEvent(s, op->ev_x[sl], 0), "wait");
+      PcgSolve ps{op, db[sl], diag, dx[sl], dinv, limit, fixed, false};
+      launched[size_t(k)] = pcg_enqueue_solve(ps, s);
+      ck(cudaMemcpyAsync(states + size_t(k) * sst, op->d_state, sizeof(PcgState),
+                         cudaMemcpyDeviceToDevice, s),
+         "state");
+      ck(cudaMemcpyAsync(hists + size_t(k) * hstride, op->w_hist.p, hstride * 8,
+                         cudaMemcpyDeviceToDevice, s),
+         "history");
+      ck(cudaEventRecord(op->ev_solved[sl], s), "event");
+      ck(cudaStreamWaitEvent(op->s_d2h, op->ev_solved[sl], 0), "wait");
+      ck(cudaMemcpyAsync(x[k], dx[sl], n * 8, cudaMemcpyDeviceToHost, op->s_d2h), "D2H x");
+      ck(cudaEventRecord(op->ev_x[sl], op->s_d2h), "event");
+    }
+    ck(cudaStreamWaitEvent(s, op->ev_x[(nrhs - 1) & 1], 0), "wait");
+    ck(cudaEventRecord(op->ev_t1, s), "event");
+    ck(cudaStreamSynchronize(s), "pcg batch");
+    ck(cudaStreamSynchronize(op->s_d2h), "pcg batch");
+    std::vector<PcgState> hs(static_cast<size_t>(nrhs));
+    for (int k = 0; k < nrhs; ++k)
+      ck(cudaMemcpy(&hs[size_t(k)], states + size_t(k) * sst, sizeof(PcgState),
+                    cudaMemcpyDeviceToHost),
+         "state");
+    float tot = 0;
+    ck(cudaEventElapsedTime(&tot, op->ev_t0, op->ev_t1), "elapsed");
+    for (int k = 0; k < nrhs; ++k) {
+      pcg_fill_report(op, hs[size_t(k)], hists + size_t(k) * hstride, launched[size_t(k)], false,
+                      &reports[k]);
+      reports[k].total_time_seconds = tot * 1e-3 / nrhs;  // batch wall share (device events)
+    }
   });
 }
 

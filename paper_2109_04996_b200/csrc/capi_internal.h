@@ -92,9 +92,20 @@ struct hxf_op {
   PcgState* d_state = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;  // cached fixed-iteration PCG graph
-  std::vector<const void*> graph_key;
-  int64_t graph_kernels = 0;
+  struct Graph {  // cached fixed-iteration PCG graph for one operand set
+    std::vector<const void*> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  };
+  std::vector<Graph> graphs;
+  void drop_graphs() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
+  // pipelined host batches (hxf_pcg_host_batch): copy streams, slot events
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_b[2] = {}, ev_solved[2] = {}, ev_x[2] = {};
+  DevVec w_b2, w_x2, w_states, w_hists;
   // partitioned box (hxf_operator_set_partition): the communicator, the
   // subdomains sharing this lattice's low / high face plane per axis, the
   // owner mask over scalar nodes (dots) and plane staging buffers
@@ -123,10 +134,15 @@ struct hxf_op {
                       (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state, (void*)d_own})
       if (ptr) cudaFree(ptr);
     for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
-                      &w_ldiag, &w_halo})
+                      &w_ldiag, &w_halo, &w_b2, &w_x2, &w_states, &w_hists})
       v->release();
     for (auto e : ev) cudaEventDestroy(e);
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    drop_graphs();
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_b[k], ev_solved[k], ev_x[k]})
+        if (e) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
     if (ev_t0) cudaEventDestroy(ev_t0);
     if (ev_t1) cudaEventDestroy(ev_t1);
   }

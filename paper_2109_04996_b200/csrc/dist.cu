@@ -466,11 +466,7 @@ int hxf_operator_set_partition(hxf_op* op, hxf_comm* comm, const hxf_partition_d
     ck(cudaMemcpy(op->d_own, own.data(), own.size() * 4, cudaMemcpyHostToDevice), "owner upload");
     op->comm = comm->impl.get();
     std::memcpy(op->neighbor, desc->neighbor, sizeof op->neighbor);
-    if (op->graph_exec) {
-      cudaGraphExecDestroy(op->graph_exec);
-      op->graph_exec = nullptr;
-      op->graph_key.clear();
-    }
+    op->drop_graphs();
   });
 }
 

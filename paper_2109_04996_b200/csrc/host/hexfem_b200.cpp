@@ -415,6 +415,29 @@ SolveReport Operator::pcg(const double* b, const double* diag, const hxf_pcg_opt
   return out;
 }
 
+std::vector<SolveReport> Operator::pcg_host_batch(const std::vector<const double*>& b,
+                                                  const double* diag, const hxf_pcg_options& o,
+                                                  const std::vector<double*>& x) const {
+  if (b.size() != x.size()) throw std::invalid_argument("pcg_host_batch: b / x count mismatch");
+  const int cap = (o.fixed_iterations >= 0 ? o.fixed_iterations : o.max_iter) + 2;
+  std::vector<std::vector<double>> hist(b.size(), std::vector<double>(size_t(std::max(cap, 1))));
+  std::vector<hxf_solve_report> rep(b.size());
+  for (size_t k = 0; k < b.size(); ++k) {
+    rep[k].residual_history = hist[k].data();
+    rep[k].history_capacity = cap;
+  }
+  check(hxf_pcg_host_batch(op_, int(b.size()), b.data(), diag, &o, x.data(), rep.data()));
+  std::vector<SolveReport> out(b.size());
+  for (size_t k = 0; k < b.size(); ++k) {
+    out[k].iterations = rep[k].iterations;
+    out[k].converged = rep[k].converged != 0;
+    out[k].residual_history.assign(hist[k].begin(),
+                                   hist[k].begin() + std::min(cap, rep[k].iterations + 1));
+    out[k].total_time_seconds = rep[k].total_time_seconds;
+  }
+  return out;
+}
+
 // ------------------------------------------------------------ BP tables
 const char* bp_name(BpId bp) {
   static const char* names[] = {"?", "bp1", "bp2", "bp3", "bp4", "bp5", "bp6"};

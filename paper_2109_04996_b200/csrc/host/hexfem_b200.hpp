@@ -194,6 +194,10 @@ class Operator {
   void set_partition(const Communicator& comm, const Subdomain& sd) const;
   SolveReport pcg(const double* b, const double* diag, const hxf_pcg_options& o, double* x,
                   hxf_memspace space) const;
+  // pipelined consecutive solves from host vectors (hxf_pcg_host_batch)
+  std::vector<SolveReport> pcg_host_batch(const std::vector<const double*>& b, const double* diag,
+                                          const hxf_pcg_options& o,
+                                          const std::vector<double*>& x) const;
 
  private:
   std::shared_ptr<Device> dev_;

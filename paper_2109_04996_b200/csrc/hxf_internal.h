@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hxf.h"
@@ -97,9 +98,29 @@ int num_sms();
 // "generic" -> 2 (op_kernel.cuh only).
 int op_kernel_choice();
 bool pencil_disabled();
+bool pdl_enabled();           // HXF_PDL=1: programmatic dependent launch (off by default)
 bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward
 int dmma_warps();  // HXF_DMMA_NW: warps per element of op_dmma_kernel (2, 4 default, 8)
 int ablate_bits();
 void count_launch(int n = 1);
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; it must pdl_wait() before touching anything
+// the predecessor writes.  Only for single-wave grids that also pdl_trigger().
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace hxf

@@ -68,7 +68,6 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_scratch[NT / 32 + 1];
-  if (prm.stop && *prm.stop) return;
 
   const int tid = threadIdx.x;
   const int w = tid >> 5, l = tid & 31, g = l >> 2, t = l & 3;
@@ -97,11 +96,20 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     mbar_arrive_expect_tx(&qbar, (uint32_t)(T::QDS * 8));
     bulk_g2s(sQD, prm.qd + elem(e) * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);
   };
+  // the first element's factors do not depend on the previous kernel: request
+  // them before the PDL wait so the copy overlaps that kernel's tail
+  const bool first_qd = (int64_t)blockIdx.x < nsteps && !(prm.ablate & 4);
   if (tid == 0) {
     mbar_init(&qbar, 1);
     fence_mbar_init();
     policy = l2_evict_first_policy();
-    if ((int64_t)blockIdx.x < nsteps && !(prm.ablate & 4)) issue_qdata(blockIdx.x);
+    if (first_qd) issue_qdata(blockIdx.x);
+  }
+  pdl_wait();     // x, y, stop and the PCG state come from the previous kernels
+  // (no early trigger: dependents launch when this grid completes)
+  if (prm.stop && *prm.stop) {
+    if (tid == 0 && first_qd) mbar_wait(&qbar, 0);  // no copy in flight at exit
+    return;
   }
 
   // Gather geometry of one element for this lane: node of (i = 2t, j = g,

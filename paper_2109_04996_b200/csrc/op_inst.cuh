@@ -92,9 +92,9 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   const int grid = (int)(prm.E < max_ctas ? prm.E : max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm);
+  const cudaError_t err = launch_pdl(kern, dim3(grid), dim3(T::NT), T::SMEM_BYTES, s, prm);
   count_launch();
-  return cudaGetLastError();
+  return err;
 }
 
 template <int NC, int NW>

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
                       double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                       const double* __restrict__ Ap, const uint32_t* own, double* part, int rev) {
   __shared__ double scratch[VT / 32];
+  pdl_wait();
   if (st->stop) return;
   const double pap = st->red[0];
   const double rho = st->rho;
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(VT, 4)
                          double* __restrict__ p, double* __restrict__ Ap,
                          const uint32_t* cons_mask, const uint32_t* own, double* part, int rev) {
   __shared__ double scratch[VT / 32];
+  pdl_wait();
   if (st->stop) return;
   const double rr = st->red[1], rz = st->red[2];
   const double res = sqrt(rr);
@@ -367,22 +369,21 @@ cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L,
                    aligned16(p) && aligned16(Ap);
   auto k = vec ? (own ? pcg_update_kernel<true, true> : pcg_update_kernel<true, false>)
                : (own ? pcg_update_kernel<false, true> : pcg_update_kernel<false, false>);
-  k<<<vec_grid(), VT, 0, s>>>(st, it, n_L, m, d, x, r, p, Ap, own, part, rev);
+  const cudaError_t err =
+      launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, n_L, m, d, x, r, p, Ap, own, part, rev);
   count_launch();
-  return cudaGetLastError();
+  return err;
 }
 
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
                                  int m, const double* d, const double* r, double* p, double* Ap,
                                  const uint32_t* mask, const uint32_t* own, double* part, int rev) {
-  if ((n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap))
-    pcg_direction_kernel<true><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
-                                                        own, part, rev);
-  else
-    pcg_direction_kernel<false><<<vec_grid(), VT, 0, s>>>(st, it, hist, n_L, m, d, r, p, Ap, mask,
-                                                         own, part, rev);
+  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap);
+  auto k = vec ? pcg_direction_kernel<true> : pcg_direction_kernel<false>;
+  const cudaError_t err = launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, hist, n_L, m, d,
+                                     r, p, Ap, mask, own, part, rev);
   count_launch();
-  return cudaGetLastError();
+  return err;
 }
 
 }  // namespace hxf

@@ -132,3 +132,25 @@ def test_errors_map_to_reference_exceptions():
     p = hx.setup("bp3", degree=2, dims=(1, 1, 1))
     with pytest.raises(ValueError):
         p.apply(np.zeros(3))
+
+
+def test_pcg_host_batch_matches_single_solves():
+    """hxf_pcg_host_batch (pipelined copies) == hxf_pcg per right-hand side."""
+    import torch
+    import paper_2109_04996_b200 as hx
+
+    pr = hx.setup("bp5", degree=4, dims=(4, 3, 3), deform="sine")
+    n = pr.size
+    rng = np.random.default_rng(3)
+    bs = [torch.from_numpy(rng.uniform(-1, 1, n)).pin_memory() for _ in range(5)]
+    xs = [torch.zeros(n, dtype=torch.float64).pin_memory() for _ in range(5)]
+    for kw in ({"fixed_iterations": 17}, {"tol": 1e-9}):
+        reps = pr.pcg_host_batch([b.data_ptr() for b in bs], [x.data_ptr() for x in xs], **kw)
+        for b, x, rep in zip(bs, xs, reps):
+            x1 = torch.zeros(n, dtype=torch.float64)
+            rep1 = pr.pcg_host(b.data_ptr(), x1.data_ptr(), **kw)
+            assert abs(rep["iterations"] - rep1["iterations"]) <= 1
+            assert oracle.rel_max_diff(x1.numpy(), x.numpy()) <= 1e-10
+            k = min(len(rep["residual_history"]), len(rep1["residual_history"]))
+            assert oracle.rel_max_diff(rep1["residual_history"][:k],
+                                       rep["residual_history"][:k]) <= 1e-10
