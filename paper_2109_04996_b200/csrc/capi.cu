@@ -113,6 +113,14 @@ bool pdl_enabled() {  // measured neutral in the CG graph at C3: opt-in
   return on;
 }
 
+bool overlap_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_OVERLAP");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 bool serpentine() {
   static const bool on = [] {
     const char* v = std::getenv("HXF_SERPENTINE");
@@ -186,13 +194,11 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.rev = rev;
   const int last_pass = op->beta != 0.0 ? 1 : 0;
   int total = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    const double coef = pass == 0 ? op->alpha : op->beta;
-    if (coef == 0.0) continue;
+  auto launch = [&](int pass, double coef, PcgState* fin_st) {
     prm.qd = pass == 0 ? op->d_qd_diff : op->d_qd_mass;
     prm.coef = coef;
     prm.dot_partials = dot_part ? dot_part + total : nullptr;
-    prm.fin = PcgAlphaFin{pass == last_pass ? st : nullptr, dot_part, total};
+    prm.fin = PcgAlphaFin{fin_st, dot_part, total};
     int grid = 0;
     const cudaError_t err = launch_op(op->P, op->Q, op->m, op->interp, pass == 0 ? 1 : 2, prm,
                                       op->B.data(), op->Dq.data(), s, &grid);
@@ -200,6 +206,32 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
       fail(HXF_EUNSUPPORTED, "operator kernel not instantiated for this (p, q, m)");
     ck(err, "operator kernel launch");
     total += grid;
+  };
+  // partitioned, one diffusion pass on the DMMA kernel: boundary elements,
+  // fork the sum-exchange of the interface planes (only boundary elements
+  // touch them) onto the comm stream, interior elements meanwhile, join
+  const bool split = halo && op->comm && op->d_elist && op->n_bnd > 0 && op->n_int > 0 &&
+                     op->beta == 0.0 && op->P == 8 && !op->interp && op_kernel_choice() == 0 &&
+                     overlap_enabled();
+  if (split) {
+    prm.elist = op->d_elist;
+    prm.E = op->n_bnd;
+    launch(0, op->alpha, nullptr);
+    ck(cudaEventRecord(op->ev_fork, s), "fork");
+    prm.elist = op->d_elist + op->n_bnd;
+    prm.E = op->n_int;
+    launch(0, op->alpha, st);
+    ck(cudaStreamWaitEvent(op->s_comm, op->ev_fork, 0), "fork");
+    op_halo_sum(op, y, op->s_comm);
+    ck(cudaEventRecord(op->ev_join, op->s_comm), "join");
+    ck(cudaStreamWaitEvent(s, op->ev_join, 0), "join");
+    if (nparts) *nparts = total;
+    return;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const double coef = pass == 0 ? op->alpha : op->beta;
+    if (coef == 0.0) continue;
+    launch(pass, coef, pass == last_pass ? st : nullptr);
   }
   if (nparts) *nparts = total;
   if (halo) op_halo_sum(op, y, s);  // partitioned: assemble interface rows (else no-op)
@@ -341,10 +373,11 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
   int nparts = 0;
   if (ps.timed) record(op->ev[2 * (it - 1)]);
   // Ap was preset by the init / direction kernel: no memset pass here
+  // partitioned: the interface sum-exchange of Ap is part of the apply
+  // (overlapped with the interior elements where the kernel allows)
   device_apply(op, p, Ap, s, op->d_part, &nparts, &op->d_state->stop, /*zero_y=*/false,
-               op->d_state, /*halo=*/false, serp & (odd ^ 1));
-  if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time = the operator kernel alone
-  op_halo_sum(op, Ap, s);                          // partitioned: assemble interface rows
+               op->d_state, /*halo=*/true, serp & (odd ^ 1));
+  if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time (single GPU: K1 alone)
   op_allreduce(op, red, 1, s);                     // pAp
   ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, ps.dinv, ps.dx, r, p, Ap, op->d_own,
                        vpart, serp & odd),

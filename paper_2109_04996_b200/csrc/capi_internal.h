@@ -113,6 +113,12 @@ struct hxf_op {
   int neighbor[3][2] = {{-1, -1}, {-1, -1}, {-1, -1}};
   uint32_t* d_own = nullptr;
   DevVec w_halo;
+  // boundary-first apply: elements touching an interface plane, then the
+  // rest, while the sum-exchange runs on a high-priority stream
+  int* d_elist = nullptr;
+  int64_t n_bnd = 0, n_int = 0;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   int64_t size() const { return int64_t(m) * n_L; }
   Lattice lattice() const {
@@ -131,7 +137,7 @@ struct hxf_op {
   ~hxf_op() {
     for (void* ptr : {(void*)d_idx, (void*)d_mask, (void*)d_qd_diff, (void*)d_qd_mass,
                       (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
-                      (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state, (void*)d_own})
+                      (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state, (void*)d_own, (void*)d_elist})
       if (ptr) cudaFree(ptr);
     for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
                       &w_ldiag, &w_halo, &w_b2, &w_x2, &w_states, &w_hists})
@@ -142,6 +148,9 @@ struct hxf_op {
       for (cudaEvent_t e : {ev_b[k], ev_solved[k], ev_x[k]})
         if (e) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_comm) cudaStreamDestroy(s_comm);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (s_d2h) cudaStreamDestroy(s_d2h);
     if (ev_t0) cudaEventDestroy(ev_t0);
     if (ev_t1) cudaEventDestroy(ev_t1);
@@ -155,6 +164,7 @@ void op_halo_sum(hxf_op* op, double* v, cudaStream_t s);
 void op_allreduce(hxf_op* op, double* dev, int n, cudaStream_t s);
 bool op_partitioned(const hxf_op* op);
 bool op_graph_safe(const hxf_op* op);
+bool overlap_enabled();  // HXF_OVERLAP=0: exchange after the whole apply
 void set_last_error(const char* msg);  // capi.cu: the thread's hxf_last_error()
 void op_set_constrained(hxf_op* op, double* v, double value, cudaStream_t s);
 }  // namespace hxf

@@ -464,6 +464,35 @@ int hxf_operator_set_partition(hxf_op* op, hxf_comm* comm, const hxf_partition_d
             own[size_t(node >> 5)] |= 1u << (node & 31);
     if (!op->d_own) op->d_own = dalloc<uint32_t>(own.size());
     ck(cudaMemcpy(op->d_own, own.data(), own.size() * 4, cudaMemcpyHostToDevice), "owner upload");
+    // boundary-first element order: elements with a face on an interface
+    // plane (the only writers of shared nodes), then the interior
+    std::vector<int> bnd, inr;
+    const int nx = op->nx, ny = op->ny, nz = op->nz;
+    const int(*nb)[2] = desc->neighbor;
+    for (int ez = 0; ez < nz; ++ez)
+      for (int ey = 0; ey < ny; ++ey)
+        for (int ex = 0; ex < nx; ++ex) {
+          const bool b = (ex == 0 && nb[0][0] >= 0) || (ex == nx - 1 && nb[0][1] >= 0) ||
+                         (ey == 0 && nb[1][0] >= 0) || (ey == ny - 1 && nb[1][1] >= 0) ||
+                         (ez == 0 && nb[2][0] >= 0) || (ez == nz - 1 && nb[2][1] >= 0);
+          (b ? bnd : inr).push_back(ex + nx * (ey + ny * ez));
+        }
+    if (op->d_elist) cudaFree(op->d_elist);
+    op->d_elist = dalloc<int>(size_t(op->E));
+    ck(cudaMemcpy(op->d_elist, bnd.data(), bnd.size() * 4, cudaMemcpyHostToDevice), "elist");
+    ck(cudaMemcpy(op->d_elist + bnd.size(), inr.data(), inr.size() * 4, cudaMemcpyHostToDevice),
+       "elist");
+    op->n_bnd = int64_t(bnd.size());
+    op->n_int = int64_t(inr.size());
+    if (!op->s_comm) {
+      int lo = 0, hi = 0;
+      ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority");
+      // highest priority: the exchange's kernels are scheduled ahead of the
+      // interior elements' CTAs as SM slots free up
+      ck(cudaStreamCreateWithPriority(&op->s_comm, cudaStreamNonBlocking, hi), "comm stream");
+      ck(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming), "event");
+    }
     op->comm = comm->impl.get();
     std::memcpy(op->neighbor, desc->neighbor, sizeof op->neighbor);
     op->drop_graphs();

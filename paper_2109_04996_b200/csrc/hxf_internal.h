@@ -53,6 +53,7 @@ struct OpParams {
   const double* D;           // device copy of the 1-D derivative matrix (collocated path)
   PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
   int rev;                   // sweep elements last to first (L2 reuse across CG kernels)
+  const int* elist;          // element ids to process (E entries), nullptr = 0..E-1 (DMMA kernel)
 };
 
 // Is lattice node (ix, iy, iz) on a constrained face of the box (mode 1)?

@@ -91,7 +91,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   // sweep position -> element: last to first when prm.rev (the CG driver
   // alternates sweep directions so each kernel starts where the previous one's
   // most recent, L2-resident, vector traffic is)
-  auto elem = [&](int64_t e) { return prm.rev ? nsteps - 1 - e : e; };
+  auto elem = [&](int64_t s) {
+    const int64_t k = prm.rev ? nsteps - 1 - s : s;
+    return prm.elist ? (int64_t)__ldg(prm.elist + k) : k;  // subset (partition overlap)
+  };
   auto issue_qdata = [&](int64_t e) {
     mbar_arrive_expect_tx(&qbar, (uint32_t)(T::QDS * 8));
     bulk_g2s(sQD, prm.qd + elem(e) * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);

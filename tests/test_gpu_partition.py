@@ -27,6 +27,11 @@ CASES = [
     ("bp1", 3, (4, 2, 2), "sine", 2),
     ("bp2", 2, (3, 2, 2), "none", 3),
     ("bp4", 2, (4, 2, 2), "sine", 2),
+    # p = 7 collocated: the DMMA kernel's boundary-first split, the exchange
+    # forked onto the comm stream while the interior elements compute
+    ("bp5", 7, (6, 4, 4), "sine", 4),
+    ("bp6", 7, (6, 3, 3), "sine", 2),
+    ("bp5", 7, (4, 4, 4), "none", 8),
 ]
 
 
@@ -77,7 +82,8 @@ def test_partitioned_apply_diag_rhs(bp, p, dims, deform, nranks):
         assert oracle.rel_max_diff(rhs_g[idx], rhs) <= 1e-12
 
 
-@pytest.mark.parametrize("bp,p,dims,deform,nranks", [CASES[0], CASES[1], CASES[3], CASES[4]])
+@pytest.mark.parametrize("bp,p,dims,deform,nranks",
+                         [CASES[0], CASES[1], CASES[3], CASES[4], CASES[7], CASES[8]])
 def test_partitioned_pcg(bp, p, dims, deform, nranks):
     g = _core.setup(bp, p, dims, deform)
     xg, rep_g = g.solve(tol=1e-8)
