@@ -243,13 +243,14 @@ def run_reference(args):
     t = sum(times)
     value = prob.n * iters * len(times) / t / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (manufactured sin(pi x) sin(pi y) sin(pi z) RHS on the sine-deformed box)",
         "config": {"workload": f"{args.bp} p={args.degree} {args.elems}^3 {args.deform}, "
                                f"Jacobi-PCG {iters} fixed iterations per step",
-                   "n_dofs": prob.n, "threads": cores},
+                   "n_dofs": prob.n, "threads": cores,
+                   "note": "host CPU only; rank 0 runs one per-GPU sub-box sample"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"reference Problem.solve, {iters} fixed CG iterations per "
                                    f"step, PCG timer (pcg.cpp:33-113)"},

@@ -5,6 +5,7 @@
 #include "op_kernel.cuh"
 #include "op_pencil.cuh"
 #include "op_dmma.cuh"
+#include "op_line.cuh"
 
 namespace hxf {
 namespace {
@@ -22,6 +23,35 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
                 int* grid_out) {
   static int max_ctas = -1;
   auto kern = op_apply_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  OpMats<T::P, T::Q> mats;
+  std::memset(&mats, 0, sizeof mats);
+  if (T::INTERP) std::memcpy(mats.B, B, sizeof(double) * T::Q * T::P);
+  std::memcpy(mats.D, D, sizeof(double) * T::Q * T::Q);
+  const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
+  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Line kernel (op_line.cuh): interpolating bases and the large collocated sizes.
+template <class T>
+cudaError_t run_line(const OpParams& prm, const double* B, const double* D, cudaStream_t s,
+                     int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_line_kernel<T>;
   if (max_ctas < 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            T::SMEM_BYTES);
@@ -140,6 +170,12 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
       return run_pencil_gm<P, 1>(prm, D, s, g);
     if (qk == 1 && NC == 3 && use_pencil<P, 3>() && !pencil_disabled())
       return run_pencil_gm<P, 3>(prm, D, s, g);
+  }
+  if (op_kernel_choice() != 2) {
+    if (NC == 1 && qk == 1) return run_line<LineTraits<P, Q, 1, 1, INTERP>>(prm, B, D, s, g);
+    if (NC == 1 && qk == 2) return run_line<LineTraits<P, Q, 1, 2, INTERP>>(prm, B, D, s, g);
+    if (NC == 3 && qk == 1) return run_line<LineTraits<P, Q, 3, 1, INTERP>>(prm, B, D, s, g);
+    if (NC == 3 && qk == 2) return run_line<LineTraits<P, Q, 3, 2, INTERP>>(prm, B, D, s, g);
   }
   if (NC == 1 && qk == 1) return run<typename Pick<P, Q, 1, INTERP, 1>::T>(prm, B, D, s, g);
   if (NC == 1 && qk == 2) return run<typename Pick<P, Q, 1, INTERP, 2>::T>(prm, B, D, s, g);
