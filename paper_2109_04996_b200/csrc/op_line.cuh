@@ -34,16 +34,25 @@
 
 namespace hxf {
 
-template <int P_, int Q_, int NC_, int QK_, bool INTERP_>
+template <int P_, int Q_, int NC_, int QK_, bool INTERP_, bool DOT_ = false>
 struct LineTraits {
   static constexpr int P = P_, Q = Q_, NC = NC_, QK = QK_;
+  // contraction order: axpy (independent accumulators) or dot; measured
+  // equal at q = 9, 12, 14
+  static constexpr bool DOT = DOT_;
+  // z-derivative / v2 of the column kept in registers across phases 4-7
+  // (measured faster at q = 9); larger q recompute it from S2 in phase 5
+  static constexpr bool EARLY = Q <= 12 || Q >= 16;
   static constexpr bool INTERP = INTERP_;
   static constexpr bool DIFF = QK == 1;  // one qdata kind per launch (1 diffusion, 2 mass)
   static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
   static constexpr int EPB = QQ >= 64 ? 1 : (128 / QQ);
   static constexpr int NT = round_up(EPB * QQ, 32);
   static constexpr int MINB = (65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128) > 8 ? 8 : 65536 / (NT * 128));
-  static constexpr int RS = Q | 1;        // odd row stride: x-line reads conflict-free
+  // odd row stride: x-line (stride RS across lanes) and column / y-line
+  // (consecutive across lanes) accesses are all conflict-free (measured: a
+  // 16-byte aligned RS = 2 mod 4 with LDS.128 x-lines is 20 % slower at q = 9)
+  static constexpr int RS = Q | 1;
   static constexpr int SLAB = Q * Q * RS;
   static constexpr int NQD = DIFF ? 6 : 1;
   static constexpr int QDS = round_up(NQD * Q3, 2);  // padded doubles per element
@@ -77,6 +86,90 @@ __device__ __forceinline__ void line_row(const double* src, double* d) {
     d[a + 1] = v.y;
   }
   if (N & 1) d[N - 1] = src[N - 1];
+}
+
+// out[o] = sum_a M[o][a] in[a] (o < NO, a < NI) in "axpy" order: column a of
+// M is the contiguous shared-memory row mt + a*str (broadcast LDS.128), so the
+// NO accumulators are independent chains; each sum still runs over a in
+// increasing order (contraction.cpp:26-73).
+template <int NI, int NO>
+__device__ __forceinline__ void line_contract(const double* mt, int str, const double* in,
+                                              double* out) {
+#pragma unroll
+  for (int o = 0; o < NO; ++o) out[o] = 0.0;
+#pragma unroll
+  for (int a = 0; a < NI; ++a) {
+    double col[NO];
+    line_row<NO>(mt + a * str, col);
+#pragma unroll
+    for (int o = 0; o < NO; ++o) out[o] += col[o] * in[a];
+  }
+}
+
+// the same contraction in "dot" order: row o of M is the shared-memory row
+// m + o*str (one dependent chain per output)
+template <int NI, int NO>
+__device__ __forceinline__ void line_contract_dot(const double* m, int str, const double* in,
+                                                  double* out) {
+#pragma unroll
+  for (int o = 0; o < NO; ++o) {
+    double row[NI];
+    line_row<NI>(m + o * str, row);
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < NI; ++a) s += row[a] * in[a];
+    out[o] = s;
+  }
+}
+
+template <bool DOT, int NI, int NO>
+__device__ __forceinline__ void lc(const double* colm, int cstr, const double* rowm, int rstr,
+                                   const double* in, double* out) {
+  if constexpr (DOT)
+    line_contract_dot<NI, NO>(rowm, rstr, in, out);
+  else
+    line_contract<NI, NO>(colm, cstr, in, out);
+}
+
+// a contiguous slab line (x-line) to / from registers
+template <int N>
+__device__ __forceinline__ void ld_line(const double* src, double* d) {
+#pragma unroll
+  for (int a = 0; a < N; ++a) d[a] = src[a];
+}
+template <int N>
+__device__ __forceinline__ void st_line(double* dst, const double* d) {
+#pragma unroll
+  for (int a = 0; a < N; ++a) dst[a] = d[a];
+}
+
+// Phases 4 / 6: the x-line (b, a, :) of sx and the y-line (b, :, a) of sy
+// through the same Q x Q matrix M (rows m + o*RQ), one broadcast row load
+// feeding both lines; results to the same lines of dx / dy (in place safe:
+// both lines are read before the first write).
+template <class T>
+__device__ __forceinline__ void line_pair(const double* m, const double* sx, const double* sy,
+                                          double* dx, double* dy, int a, int b) {
+  constexpr int Q = T::Q;
+  double lx[Q], ly[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    lx[i] = sx[T::off(b, a, i)];
+    ly[i] = sy[T::off(b, i, a)];
+  }
+#pragma unroll
+  for (int o = 0; o < Q; ++o) {
+    double row[Q];
+    line_row<Q>(m + o * T::RQ, row);
+    double px = 0.0, py = 0.0;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      px += row[i] * lx[i];
+      py += row[i] * ly[i];
+    }
+    dx[T::off(b, a, o)] = px;
+    dy[T::off(b, o, a)] = py;
+  }
 }
 
 template <class T>
@@ -183,7 +276,6 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
     const bool eactive = aslot && e < prm.E;
     const double* qd_el = prm.qd + (eactive ? e : 0) * T::QDS;
     if (tid == 0) prefetch_qd(step + G);
-    const LineGeo gnext = geometry(step + G);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       double* yc = prm.y + c * prm.n_L;
@@ -194,35 +286,22 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
       for (int n = 0; n < P; ++n) u[n] = (gcur.active && !((gcur.cmask >> n) & 1u)) ? xn[n] : 0.0;
 
       double uq[Q];  // u at the quadrature points of this thread's column
-      double g2[Q];  // z-derivative of the column, then v2
       if constexpr (T::INTERP) {
-        // ---- 1: x-interp of the gathered x-line ----
+        // ---- 1: x-interp of the gathered x-line -> S0 [k][j][qi] ----
         if (gthread) {
-#pragma unroll
-          for (int o = 0; o < Q; ++o) {
-            double mrow[P];
-            line_row<P>(sB + o * T::RP, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < P; ++a) s += mrow[a] * u[a];
-            S0[T::off(pb, pa, o)] = s;
-          }
+          double t[Q];
+          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, u, t);
+          st_line<Q>(S0 + T::off(pb, pa, 0), t);
         }
         __syncthreads();
-        // ---- 2: y-interp, line (qi, k) ----
+        // ---- 2: y-interp, line (qi, k) -> S1 [k][qj][qi] ----
         if (aslot && l < Q * P) {
-          double ln[P];
+          double ln[P], t[Q];
 #pragma unroll
           for (int b = 0; b < P; ++b) ln[b] = S0[T::off(qb, b, qa)];
+          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, ln, t);
 #pragma unroll
-          for (int o = 0; o < Q; ++o) {
-            double mrow[P];
-            line_row<P>(sB + o * T::RP, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int b = 0; b < P; ++b) s += mrow[b] * ln[b];
-            S1[T::off(qb, o, qa)] = s;
-          }
+          for (int o = 0; o < Q; ++o) S1[T::off(qb, o, qa)] = t[o];
         }
         __syncthreads();
         // ---- 3: z-interp of the column (qi, qj) ----
@@ -230,73 +309,58 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
           double ln[P];
 #pragma unroll
           for (int k = 0; k < P; ++k) ln[k] = aslot ? S1[T::off(k, qb, qa)] : 0.0;
-#pragma unroll
-          for (int o = 0; o < Q; ++o) {
-            double mrow[P];
-            line_row<P>(sB + o * T::RP, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int k = 0; k < P; ++k) s += mrow[k] * ln[k];
-            uq[o] = s;
-          }
+          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, ln, uq);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < Q; ++k) uq[k] = u[k < P ? k : 0];
       }
-      // next item's raw line
-      {
-        const LineGeo gn = c + 1 < NC ? gcur : gnext;
-        load_line(gn, (c + 1) % NC, xn);
+      // next item's raw line (geometry recomputed at the step end: fewer
+      // registers live across the phases)
+      if (c + 1 < NC) {
+        load_line(gcur, c + 1, xn);
+      } else {
+        load_line(geometry(step + G), 0, xn);
       }
 
       double energy = 0.0;
       double w[Q];
+      double g2[T::EARLY ? Q : 1];  // EARLY: z-derivative, then v2, of the column
       if constexpr (T::DIFF) {
         if (aslot) {
 #pragma unroll
           for (int k = 0; k < Q; ++k) S2[T::off(k, qb, qa)] = uq[k];
         }
-#pragma unroll
-        for (int o = 0; o < Q; ++o) {
-          double mrow[Q];
-          line_row<Q>(sD + o * T::RQ, mrow);
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < Q; ++k) s += mrow[k] * uq[k];
-          g2[o] = s;
-        }
+        if constexpr (T::EARLY) lc<T::DOT, Q, Q>(sDT, T::RQ, sD, T::RQ, uq, g2);
         __syncthreads();
         // ---- 4: x and y derivatives, thread (a, b) = (qa, qb) ----
         if (aslot) {
-          double lx[Q], ly[Q];
-#pragma unroll
-          for (int i = 0; i < Q; ++i) {
-            lx[i] = S2[T::off(qb, qa, i)];
-            ly[i] = S2[T::off(qb, i, qa)];
-          }
-#pragma unroll
-          for (int o = 0; o < Q; ++o) {
-            double mrow[Q];
-            line_row<Q>(sD + o * T::RQ, mrow);  // one row feeds both lines
-            double sx = 0.0, sy = 0.0;
-#pragma unroll
-            for (int i = 0; i < Q; ++i) {
-              sx += mrow[i] * lx[i];
-              sy += mrow[i] * ly[i];
-            }
-            S0[T::off(qb, qa, o)] = sx;
-            S1[T::off(qb, o, qa)] = sy;
-          }
+          line_pair<T>(sD, S2, S2, S0, S1, qa, qb);
         }
         __syncthreads();
-        // ---- 5: QFunction on the column (qfunction.cpp:135-162) ----
+        // ---- 5: z-derivative of the column (still in S2) + QFunction
+        //      (qfunction.cpp:135-162); v2 replaces the column in S2 ----
         if (aslot) {
+          double ln[T::EARLY ? 1 : Q];
+          if constexpr (!T::EARLY) {
 #pragma unroll
+            for (int k = 0; k < Q; ++k) ln[k] = S2[T::off(k, qb, qa)];
+          }
+          // (late form: partial unroll, two points' factors in flight)
+#pragma unroll (T::EARLY ? Q : 2)
           for (int k = 0; k < Q; ++k) {
             const int sp = T::off(k, qb, qa);
             const int pt = k * QQ + qb * Q + qa;
-            const double a0 = S0[sp], a1 = S1[sp], a2 = g2[k];
+            double a2 = 0.0;  // z-derivative at point k
+            if constexpr (T::EARLY) {
+              a2 = g2[k];
+            } else {  // row k of D . column
+              double mrow[Q];
+              line_row<Q>(sD + k * T::RQ, mrow);
+#pragma unroll
+              for (int c2 = 0; c2 < Q; ++c2) a2 += mrow[c2] * ln[c2];
+            }
+            const double a0 = S0[sp], a1 = S1[sp];
             double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
             if (eactive) {
               s00 = ld_stream(qd_el + 0 * Q3 + pt);
@@ -311,44 +375,35 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             const double v2 = s02 * a0 + s12 * a1 + s22 * a2;
             S0[sp] = v0;
             S1[sp] = v1;
-            g2[k] = v2;
+            if constexpr (T::EARLY)
+              g2[k] = v2;
+            else
+              S2[sp] = v2;
             energy += a0 * v0 + a1 * v1 + a2 * v2;
           }
         }
         __syncthreads();
         // ---- 6: x^T and y^T derivatives in place ----
         if (aslot) {
-          double lx[Q], ly[Q];
-#pragma unroll
-          for (int i = 0; i < Q; ++i) {
-            lx[i] = S0[T::off(qb, qa, i)];
-            ly[i] = S1[T::off(qb, i, qa)];
-          }
-#pragma unroll
-          for (int o = 0; o < Q; ++o) {
-            double mrow[Q];
-            line_row<Q>(sDT + o * T::RQ, mrow);  // one row feeds both lines
-            double sx = 0.0, sy = 0.0;
-#pragma unroll
-            for (int i = 0; i < Q; ++i) {
-              sx += mrow[i] * lx[i];
-              sy += mrow[i] * ly[i];
-            }
-            S0[T::off(qb, qa, o)] = sx;
-            S1[T::off(qb, o, qa)] = sy;
-          }
+          line_pair<T>(sDT, S0, S1, S0, S1, qa, qb);
         }
         __syncthreads();
         // ---- 7a: column sum with the z^T derivative ----
+        {
+          double ln[Q], t[Q];
 #pragma unroll
-        for (int o = 0; o < Q; ++o) {
-          double mrow[Q];
-          line_row<Q>(sDT + o * T::RQ, mrow);
-          double s = 0.0;
+          for (int k = 0; k < Q; ++k) {
+            if constexpr (T::EARLY)
+              ln[k] = g2[k];
+            else
+              ln[k] = aslot ? S2[T::off(k, qb, qa)] : 0.0;
+          }
+          lc<T::DOT, Q, Q>(sD, T::RQ, sDT, T::RQ, ln, t);
 #pragma unroll
-          for (int k = 0; k < Q; ++k) s += mrow[k] * g2[k];
-          const int sp = T::off(o, qb, qa);
-          w[o] = aslot ? (S0[sp] + S1[sp] + s) : 0.0;
+          for (int o = 0; o < Q; ++o) {
+            const int sp = T::off(o, qb, qa);
+            w[o] = aslot ? (S0[sp] + S1[sp] + t[o]) : 0.0;
+          }
         }
       } else {
         // mass QFunction (qfunction.cpp:124-133), column-local
@@ -365,48 +420,31 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
       if constexpr (T::INTERP) {
         // ---- 7b: z^T interp of the column -> S2 [c][qj][qi] ----
         if (aslot) {
+          double t[P];
+          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, w, t);
 #pragma unroll
-          for (int k = 0; k < P; ++k) {
-            double mrow[Q];
-            line_row<Q>(sBT + k * T::RQ, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int o = 0; o < Q; ++o) s += mrow[o] * w[o];
-            S2[T::off(k, qb, qa)] = s;
-          }
+          for (int k = 0; k < P; ++k) S2[T::off(k, qb, qa)] = t[k];
         }
         __syncthreads();
         // ---- 8: y^T interp, line (qi, k) -> S1 [k][j][qi] ----
         if (aslot && l < Q * P) {
-          double ln[Q];
+          double ln[Q], t[P];
 #pragma unroll
           for (int o = 0; o < Q; ++o) ln[o] = S2[T::off(qb, o, qa)];
+          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, ln, t);
 #pragma unroll
-          for (int j = 0; j < P; ++j) {
-            double mrow[Q];
-            line_row<Q>(sBT + j * T::RQ, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int o = 0; o < Q; ++o) s += mrow[o] * ln[o];
-            S1[T::off(qb, j, qa)] = s;
-          }
+          for (int j = 0; j < P; ++j) S1[T::off(qb, j, qa)] = t[j];
         }
         __syncthreads();
         // ---- 9: x^T interp of the x-line (j, k), RED scatter ----
         if (gcur.active) {
-          double ln[Q];
+          double ln[Q], t[P];
+          ld_line<Q>(S1 + T::off(pb, pa, 0), ln);
+          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, ln, t);
 #pragma unroll
-          for (int o = 0; o < Q; ++o) ln[o] = S1[T::off(pb, pa, o)];
-#pragma unroll
-          for (int i = 0; i < P; ++i) {
-            double mrow[Q];
-            line_row<Q>(sBT + i * T::RQ, mrow);
-            double s = 0.0;
-#pragma unroll
-            for (int o = 0; o < Q; ++o) s += mrow[o] * ln[o];
+          for (int i = 0; i < P; ++i)
             // constrained rows (y = x) are preset by the caller
-            if (!((gcur.cmask >> i) & 1u) && !(prm.ablate & 2)) red_add(yc + node_of(gcur, i), prm.coef * s);
-          }
+            if (!((gcur.cmask >> i) & 1u) && !(prm.ablate & 2)) red_add(yc + node_of(gcur, i), prm.coef * t[i]);
         }
       } else {
         // collocated: the column thread scatters its z-line
@@ -418,9 +456,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
       }
       // no trailing barrier: the next item's first shared-memory writes (S0 in
       // phase 1, S2 after phase 3) hit slabs whose last reads (phases 7a, 8)
-      // are behind at least one barrier of this item
+      // are behind at least one barrier of this item; a column of S2 is only
+      // ever rewritten by its own thread
     }
-    gcur = gnext;
+    gcur = geometry(step + G);
   }
 
   if (prm.dot_partials) {
