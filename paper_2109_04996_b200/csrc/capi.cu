@@ -105,6 +105,14 @@ int op_kernel_choice() {
 
 bool pencil_disabled() { return op_kernel_choice() == 2; }
 
+bool dmma_pad_disabled() {
+  static const bool off = [] {
+    const char* v = std::getenv("HXF_DMMA_PAD");
+    return v && v[0] == '0';
+  }();
+  return off;
+}
+
 bool pdl_enabled() {  // measured neutral in the CG graph at C3: opt-in
   static const bool on = [] {
     const char* v = std::getenv("HXF_PDL");

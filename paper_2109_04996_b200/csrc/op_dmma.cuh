@@ -34,16 +34,22 @@
 
 namespace hxf {
 
-template <int NC_, int GM_, int NW_ = 4>
+template <int NC_, int GM_, int NW_ = 4, int NP_ = 8>
 struct DmmaTraits {
   // NW warps per element; warp w owns planes / rows KK w .. KK w + KK-1
   static constexpr int P = 8, NC = NC_, GM = GM_, P3 = 512, NW = NW_, NT = 32 * NW_, KK = 8 / NW_;
+  // NP = p+1 nodes per direction: 8, or 5..7 zero-padded to the 8^3 tile
+  // (padded rows / columns of D are 0, padded points masked like constrained
+  // ones; the geometric factors stay compact, NP^3 per plane)
+  static constexpr int NP = NP_, NP3 = NP_ * NP_ * NP_;
+  static constexpr bool PAD = NP_ < 8;
+  static_assert(NP_ >= 5 && NP_ <= 8, "DMMA tile holds 5..8 nodes per direction");
   static_assert(NW_ == 2 || NW_ == 4 || NW_ == 8, "8 planes split over NW warps");
   // CTAs per SM the register budget is sized for (tuned at C3: NW = 4 -> 122
   // registers, 4 CTAs; NW = 2 needs 224 registers to keep its loads in flight)
   static constexpr int MINB = NW_ == 8 ? 3 : 4;
   static constexpr int SLAB = 512;   // doubles
-  static constexpr int QDS = 6 * P3;
+  static constexpr int QDS = 6 * NP3;
   static constexpr int OFF_QD = 0;
   static constexpr int OFF_A = QDS;  // U, then V0
   static constexpr int OFF_B = OFF_A + SLAB;  // V1, then Y2 (dist-Z -> dist-X transpose)
@@ -80,8 +86,10 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   double Dr[2], Dc[2];
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
-    Dr[ks] = __ldg(prm.D + g * 8 + ks * 4 + t);    // D[g][4ks+t]
-    Dc[ks] = __ldg(prm.D + (ks * 4 + t) * 8 + g);  // D[4ks+t][g]
+    constexpr int NP = T::NP;
+    const bool in = g < NP && ks * 4 + t < NP;
+    Dr[ks] = in ? __ldg(prm.D + g * NP + ks * 4 + t) : 0.0;    // D[g][4ks+t]
+    Dc[ks] = in ? __ldg(prm.D + (ks * 4 + t) * NP + g) : 0.0;  // D[4ks+t][g]
   }
 
   const int64_t nsteps = prm.E;
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   auto node_of = [&](const Geo& q, int kk, int h) -> int64_t {
     if constexpr (T::GM == 0) return q.key + (int64_t)kk * NXY + h;
     if (prm.idx)
-      return (int64_t)prm.idx[q.key * P3 + (2 * t + h) + 8 * (g + 8 * (KK * w + kk))];
+      return (int64_t)prm.idx[q.key * T::NP3 + (2 * t + h) + T::NP * (g + T::NP * (KK * w + kk))];
     return q.key + (int64_t)kk * NXY + h;
   };
   auto geometry = [&](int64_t s) {
@@ -137,7 +145,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       q.key = e;
     } else {
       const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      const int64_t ix = ex * 7 + 2 * t, iy = ey * 7 + g, iz = ez * 7 + KK * w;
+      const int64_t ix = ex * (T::NP - 1) + 2 * t, iy = ey * (T::NP - 1) + g,
+                    iz = ez * (T::NP - 1) + KK * w;
       q.key = ix + prm.NX * iy + NXY * iz;
       if (T::GM == 0 && prm.cons_mode == 1) {
 #pragma unroll
@@ -148,11 +157,20 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
           }
       }
     }
+    if constexpr (T::PAD) {
+      // padding points of the 8^3 tile: masked like constrained nodes
+#pragma unroll
+      for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (2 * t + h >= T::NP || g >= T::NP || KK * w + kk >= T::NP) q.cmask |= 1u << (2 * kk + h);
+    }
     if (T::GM == 1 && prm.cons_mode == 2) {
 #pragma unroll
       for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
+          if (T::PAD && ((q.cmask >> (2 * kk + h)) & 1u)) continue;
           const int64_t node = node_of(q, kk, h);
           q.cmask |= ((prm.cons_mask[node >> 5] >> (node & 31)) & 1u) << (2 * kk + h);
         }
@@ -163,7 +181,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     const double* xc = prm.x + c * prm.n_L;
     // structured box: a lane's node pair (i = 2t, 2t+1) is 16-byte aligned iff
     // its first node is even (uniform across the element when NX, n_L even)
-    if (T::GM == 0 && q.active && !(prm.ablate & 1) && ((reinterpret_cast<uintptr_t>(xc) +
+    if (T::GM == 0 && !T::PAD && q.active && !(prm.ablate & 1) && ((reinterpret_cast<uintptr_t>(xc) +
                                                          8 * q.key) & 15u) == 0 &&
         (prm.NX & 1) == 0) {
 #pragma unroll
@@ -178,7 +196,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     for (int kk = 0; kk < KK; ++kk)
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        xn[2 * kk + h] = (q.active && !(prm.ablate & 1)) ? __ldg(xc + node_of(q, kk, h)) : 1.0;
+        xn[2 * kk + h] = (q.active && !(prm.ablate & 1) && !(T::PAD && ((q.cmask >> (2 * kk + h)) & 1u)))
+                             ? __ldg(xc + node_of(q, kk, h))
+                             : 1.0;
   };
 
   Geo gcur = geometry(blockIdx.x);
@@ -254,10 +274,22 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         const int k = KK * w + kk;
         const int sp = T::off(k, g, 2 * t);
         const double2 z2 = *reinterpret_cast<const double2*>(SZ + sp);
-        const int pt = k * 64 + g * 8 + 2 * t;
         double2 s[6];
+        if constexpr (!T::PAD) {
+          const int pt = k * 64 + g * 8 + 2 * t;
 #pragma unroll
-        for (int m = 0; m < 6; ++m) s[m] = *reinterpret_cast<const double2*>(sQD + m * P3 + pt);
+          for (int m = 0; m < 6; ++m) s[m] = *reinterpret_cast<const double2*>(sQD + m * P3 + pt);
+        } else {
+          // compact NP^3 factors; padding points get 0 (their V is then 0)
+          constexpr int NP = T::NP;
+          const int pt = (k * NP + g) * NP + 2 * t;
+          const bool v0 = k < NP && g < NP && 2 * t < NP, v1 = k < NP && g < NP && 2 * t + 1 < NP;
+#pragma unroll
+          for (int m = 0; m < 6; ++m) {
+            s[m].x = v0 ? sQD[m * T::NP3 + pt] : 0.0;
+            s[m].y = v1 ? sQD[m * T::NP3 + pt + 1] : 0.0;
+          }
+        }
         double v0[2], v1[2], v2[2];
         const double gz[2] = {z2.x, z2.y};
 #pragma unroll

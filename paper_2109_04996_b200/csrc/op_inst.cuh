@@ -127,21 +127,25 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   return err;
 }
 
-template <int NC, int NW>
+template <int NC, int NW, int NP = 8>
 cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
-  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW>>(prm, s, g);
-  return run_dmma<DmmaTraits<NC, 1, NW>>(prm, s, g);
+  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW, NP>>(prm, s, g);
+  return run_dmma<DmmaTraits<NC, 1, NW, NP>>(prm, s, g);
 }
 
-template <int NC>
+template <int NC, int NP = 8>
 cudaError_t run_dmma_gm(const OpParams& prm, cudaStream_t s, int* g) {
-  switch (dmma_warps()) {
-    case 8:
-      return run_dmma_nw<NC, 8>(prm, s, g);
-    case 2:
-      return run_dmma_nw<NC, 2>(prm, s, g);
-    default:
-      return run_dmma_nw<NC, 4>(prm, s, g);
+  if constexpr (NP != 8) {
+    return run_dmma_nw<NC, 4, NP>(prm, s, g);
+  } else {
+    switch (dmma_warps()) {
+      case 8:
+        return run_dmma_nw<NC, 8>(prm, s, g);
+      case 2:
+        return run_dmma_nw<NC, 2>(prm, s, g);
+      default:
+        return run_dmma_nw<NC, 4>(prm, s, g);
+    }
   }
 }
 
@@ -160,10 +164,18 @@ template <int P, int Q, bool INTERP>
 cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const double* D,
                   cudaStream_t s, int* g) {
   if constexpr (!INTERP && P == 8) {
+    // p = 7 collocated diffusion on the FP64 tensor cores
     if (qk == 1 && op_kernel_choice() == 0) {
       if (NC == 1) return run_dmma_gm<1>(prm, s, g);
       if (NC == 3) return run_dmma_gm<3>(prm, s, g);
     }
+  }
+  if constexpr (!INTERP && P == 7) {
+    // p = 6, three components: the zero-padded 8^3 tensor-core tile beats the
+    // pencil kernel (C4 BP6 p=6 40^3: K1 833 vs 1098 us); one component and
+    // p = 4, 5 do not (fixed 8^3 tile cost per element: p=4 BP5 753 vs 297 us)
+    if (qk == 1 && NC == 3 && op_kernel_choice() == 0 && !dmma_pad_disabled())
+      return run_dmma_gm<3, P>(prm, s, g);
   }
   if constexpr (!INTERP) {
     if (qk == 1 && NC == 1 && use_pencil<P, 1>() && !pencil_disabled())

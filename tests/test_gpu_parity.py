@@ -177,7 +177,14 @@ def test_qfunction_bitwise(ctx):
                                        ("bp6", 5, (3, 3, 3)), ("bp1", 3, (6, 5, 4)),
                                        ("bp2", 4, (3, 3, 3)), ("bp4", 2, (4, 4, 4)),
                                        ("bp5", 1, (7, 6, 5)), ("bp5", 11, (2, 2, 1)),
-                                       ("bp3", 12, (1, 2, 1)), ("bp5", 15, (1, 1, 2))])
+                                       ("bp3", 12, (1, 2, 1)), ("bp5", 15, (1, 1, 2)),
+                                       # DMMA tile, zero-padded p = 4..6 and p = 7
+                                       ("bp5", 4, (3, 2, 3)), ("bp5", 5, (2, 3, 2)),
+                                       ("bp5", 6, (3, 3, 2)), ("bp6", 4, (2, 2, 3)),
+                                       ("bp6", 6, (2, 2, 2)), ("bp6", 7, (2, 3, 2)),
+                                       # line kernel sizes
+                                       ("bp3", 9, (2, 1, 2)), ("bp4", 7, (2, 2, 1)),
+                                       ("bp1", 7, (2, 2, 2)), ("bp5", 13, (1, 2, 1))])
 def test_apply_vs_oracle_across_orders(ctx, bp, p, dims):
     pr = oracle.setup(bp, p, dims, "sine")
     op = op_from_oracle(ctx, pr)
