@@ -181,8 +181,17 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
                   int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr,
                   bool halo = true, int rev = 0) {
-  if (zero_y) ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask, op->d_own), "init_y");
+  // single-domain p = 7 collocated diffusion: y zeroed by a write-only memset
+  // and the DMMA kernel stores y = x on the constrained rows it gathers
+  // (instead of the read-x/write-y init_y pass)
+  const bool cons_store = zero_y && op->P == 8 && !op->interp && op->beta == 0.0 && !op->d_own &&
+                          op->cons_mode != 0 && op_kernel_choice() == 0;
+  if (cons_store)
+    ck(cudaMemsetAsync(y, 0, sizeof(double) * op->n_L * op->m, s), "y memset");
+  else if (zero_y)
+    ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask, op->d_own), "init_y");
   OpParams prm{};
+  prm.cons_store = cons_store ? 1 : 0;
   prm.x = x;
   prm.y = y;
   prm.E = op->E;

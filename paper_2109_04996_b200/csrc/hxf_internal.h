@@ -54,6 +54,8 @@ struct OpParams {
   PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
   int rev;                   // sweep elements last to first (L2 reuse across CG kernels)
   const int* elist;          // element ids to process (E entries), nullptr = 0..E-1 (DMMA kernel)
+  int cons_store;            // DMMA kernel: store y = x on the constrained rows it gathers
+                             // (y zero-filled by the caller instead of preset by init_y)
 };
 
 // Is lattice node (ix, iy, iz) on a constrained face of the box (mode 1)?

@@ -201,6 +201,18 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
                              : 1.0;
   };
 
+  // constrained rows of a work item: y = x (operator.cpp:87-90,141-143), plain
+  // stores of the raw gathered values (idempotent across elements sharing a node)
+  auto store_cons = [&](const Geo& gq, int c, const double* raw) {
+    if (T::PAD || !prm.cons_store || !gq.active || gq.cmask == 0) return;
+    double* yc = prm.y + c * prm.n_L;
+#pragma unroll
+    for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if ((gq.cmask >> (2 * kk + h)) & 1u) yc[node_of(gq, kk, h)] = raw[2 * kk + h];
+  };
+
   Geo gcur = geometry(blockIdx.x);
   Geo gpf = NC > 1 ? gcur : geometry(blockIdx.x + G);
   double xn[2 * KK];
@@ -208,6 +220,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   double u[2 * KK];
 #pragma unroll
   for (int m = 0; m < 2 * KK; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
+  store_cons(gcur, 0, xn);
   load_lines(gpf, 1 % NC, xn);
   __syncthreads();  // mbarrier init visible
 
@@ -233,6 +246,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         for (int m = 0; m < 2 * KK; ++m) nx_[m] = xn[m];
         // masked values of item q+1 are formed when it starts (gpf)
         load_lines(gnext, (q + 2) % NC, xn);
+        store_cons(gpf, (q + 1) % NC, nx_);
 #pragma unroll
         for (int m = 0; m < 2 * KK; ++m)
           u[m] = (gpf.active && !((gpf.cmask >> m) & 1u)) ? nx_[m] : 0.0;  // item q+1
