@@ -90,6 +90,24 @@ __device__ __forceinline__ double ld_stream(const double* p) {
   return v;
 }
 
+// Division by a run-time invariant d (1 <= d < 2^31) for numerators n < 2^31
+// with one IMAD.HI + shift (round-up magic number, as in CUTLASS FastDivmod),
+// instead of the ~20-instruction integer division sequence.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  __device__ __forceinline__ explicit FastDiv(uint32_t den) : d(den), mul(0), shr(0) {
+    if (den > 1) {
+      const uint32_t l = 32 - __clz(den - 1);  // ceil(log2 den)
+      const uint32_t p = 31 + l;
+      mul = (uint32_t)(((1ull << p) + den - 1) / den);
+      shr = p - 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return mul ? (__umulhi(n, mul) >> shr) : n;
+  }
+};
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

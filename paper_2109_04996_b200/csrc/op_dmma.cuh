@@ -136,6 +136,23 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       return (int64_t)prm.idx[q.key * T::NP3 + (2 * t + h) + T::NP * (g + T::NP * (KK * w + kk))];
     return q.key + (int64_t)kk * NXY + h;
   };
+  // loop-invariant lane masks: which of this lane's points lie on each of the
+  // six faces of an element (bit 2*kk + h: point i = 2t+h, j = g, k = KK w + kk)
+  uint32_t fmask[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 2 * t + h, k = KK * w + kk;
+      const uint32_t bit = 1u << (2 * kk + h);
+      fmask[0] |= i == 0 ? bit : 0u;
+      fmask[1] |= i == T::NP - 1 ? bit : 0u;
+      fmask[2] |= g == 0 ? bit : 0u;
+      fmask[3] |= g == T::NP - 1 ? bit : 0u;
+      fmask[4] |= k == 0 ? bit : 0u;
+      fmask[5] |= k == T::NP - 1 ? bit : 0u;
+    }
+  const FastDiv divx((uint32_t)prm.nx), divy((uint32_t)prm.ny);
   auto geometry = [&](int64_t s) {
     Geo q{};
     q.active = s < nsteps;
@@ -144,17 +161,23 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     if (T::GM == 1 && prm.idx) {
       q.key = e;
     } else {
-      const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      const int64_t ix = ex * (T::NP - 1) + 2 * t, iy = ey * (T::NP - 1) + g,
-                    iz = ez * (T::NP - 1) + KK * w;
-      q.key = ix + prm.NX * iy + NXY * iz;
+      // element lattice position (E < 2^31: 32-bit fast division)
+      const uint32_t e32 = (uint32_t)e, r = divx.div(e32), ez = divy.div(r);
+      const uint32_t ex = e32 - r * (uint32_t)prm.nx, ey = r - ez * (uint32_t)prm.ny;
+      const int64_t ix0 = (int64_t)ex * (T::NP - 1), iy0 = (int64_t)ey * (T::NP - 1),
+                    iz0 = (int64_t)ez * (T::NP - 1);
+      q.key = (ix0 + 2 * t) + prm.NX * (iy0 + g) + NXY * (iz0 + KK * w);
       if (T::GM == 0 && prm.cons_mode == 1) {
-#pragma unroll
-        for (int kk = 0; kk < KK; ++kk)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (on_bnd_face(prm, ix + h, iy, iz + kk)) q.cmask |= 1u << (2 * kk + h);
-          }
+        // on_bnd_face per point, as element-face flags x lane masks
+        const int f = prm.bnd_faces;
+        uint32_t cm = 0u;
+        if ((f & 1) && ix0 == 0) cm |= fmask[0];
+        if ((f & 2) && ix0 + T::NP - 1 == prm.NX - 1) cm |= fmask[1];
+        if ((f & 4) && iy0 == 0) cm |= fmask[2];
+        if ((f & 8) && iy0 + T::NP - 1 == prm.NY - 1) cm |= fmask[3];
+        if ((f & 16) && iz0 == 0) cm |= fmask[4];
+        if ((f & 32) && iz0 + T::NP - 1 == prm.NZ - 1) cm |= fmask[5];
+        q.cmask = cm;
       }
     }
     if constexpr (T::PAD) {
@@ -226,6 +249,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
 
   double dot_acc = 0.0;
   int it = 0, q = 0;
+  Geo gnext_el{};
 #pragma unroll 1
   for (int64_t e = blockIdx.x; e < nsteps; e += G, ++it) {
 #pragma unroll 1
@@ -238,6 +262,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
             make_double2(u[2 * kk], u[2 * kk + 1]);
       // next item's raw lines: land while this item computes
       {
+        if (c == NC - 1) gnext_el = gpf;  // item q+1 starts the next element
         const Geo gnext = ((q + 2) / NC == (q + 1) / NC && NC > 1)
                               ? gpf
                               : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       }
       __syncthreads();  // (F) slab B free for the next item
     }
-    gcur = geometry(e + G);
+    gcur = gnext_el;  // == geometry(e + G), computed one item ahead
   }
 
   if (prm.dot_partials) {

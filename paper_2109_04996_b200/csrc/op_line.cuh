@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   const int64_t G = gridDim.x;
   const int64_t NXY = prm.NX * prm.NY;
 
+  const FastDiv divx((uint32_t)prm.nx), divy((uint32_t)prm.ny);
   auto geometry = [&](int64_t step) {
     LineGeo g{};
     const int64_t e = step * EPB + slot;
@@ -225,16 +226,33 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
       g.tab = e * T::P3 + li + P * (lj + P * lk);
       g.tstep = T::INTERP ? 1 : P * P;
     } else {
-      const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      const int64_t ix = ex * (P - 1) + li, iy = ey * (P - 1) + lj, iz = ez * (P - 1) + lk;
+      // element lattice position (E < 2^31: 32-bit fast division)
+      const uint32_t e32 = (uint32_t)e, r = divx.div(e32), ez = divy.div(r);
+      const uint32_t ex = e32 - r * (uint32_t)prm.nx, ey = r - ez * (uint32_t)prm.ny;
+      const int64_t ix = (int64_t)ex * (P - 1) + li, iy = (int64_t)ey * (P - 1) + lj,
+                    iz = (int64_t)ez * (P - 1) + lk;
       g.base = ix + prm.NX * iy + NXY * iz;
       g.step = T::INTERP ? 1 : NXY;
       if (prm.cons_mode == 1) {
-#pragma unroll
-        for (int n = 0; n < P; ++n) {
-          const bool c = T::INTERP ? on_bnd_face(prm, ix + n, iy, iz) : on_bnd_face(prm, ix, iy, iz + n);
-          if (c) g.cmask |= 1u << n;
+        // on_bnd_face along the line: faces across the line take all of it,
+        // the two faces it crosses take its first / last node
+        const int f = prm.bnd_faces;
+        const uint32_t all = (1u << P) - 1u;
+        uint32_t cm = 0u;
+        if (T::INTERP) {  // x-line
+          if (((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1) || ((f & 16) && iz == 0) ||
+              ((f & 32) && iz == prm.NZ - 1))
+            cm = all;
+          if ((f & 1) && ix == 0) cm |= 1u;
+          if ((f & 2) && ix + P - 1 == prm.NX - 1) cm |= 1u << (P - 1);
+        } else {  // z-line
+          if (((f & 1) && ix == 0) || ((f & 2) && ix == prm.NX - 1) || ((f & 4) && iy == 0) ||
+              ((f & 8) && iy == prm.NY - 1))
+            cm = all;
+          if ((f & 16) && iz == 0) cm |= 1u;
+          if ((f & 32) && iz + P - 1 == prm.NZ - 1) cm |= 1u << (P - 1);
         }
+        g.cmask = cm;
       }
     }
     if (prm.cons_mode == 2) {
