@@ -396,12 +396,12 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
                op->d_state, /*halo=*/true, serp & (odd ^ 1));
   if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time (single GPU: K1 alone)
   op_allreduce(op, red, 1, s);                     // pAp
-  ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, ps.dinv, ps.dx, r, p, Ap, op->d_own,
-                       vpart, serp & odd),
+  ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, ps.dinv, r, Ap, op->d_own, vpart,
+                       serp & odd),
      "pcg update");
   op_allreduce(op, red + 1, 2, s);  // r.r, r.z
-  ck(pcg_launch_direction(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, p, Ap,
-                          op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
+  ck(pcg_launch_direction(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,
+                          Ap, op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
      "pcg direction");
 }
 

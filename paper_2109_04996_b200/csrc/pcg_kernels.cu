@@ -5,13 +5,15 @@
 //   K1      Ap += A p over free rows (op_dmma / op_pencil / op_kernel); its
 //           last CTA writes this rank's pAp into red[0]
 //   update  every CTA derives alpha = rho / pAp from red[0] with the
-//           reference's checks (pcg.cpp:74-82); x += alpha p, r -= alpha Ap;
+//           reference's checks (pcg.cpp:74-82); r -= alpha Ap;
 //           last CTA: red[1] = r.r, red[2] = r.(r/d) over owned rows
-//   dir     every CTA derives ||r||, convergence / limit (pcg.cpp:90-99) and
-//           beta = rho' / rho from red[1..2]; p = r/d + beta p;
-//           Ap = (constrained & owned ? p : 0), the next RED target; last CTA
-//           records the iteration and red[3] = sum of p^2 over owned
-//           constrained rows
+//   dir     x += alpha p (pcg.cpp:84-88: moved here, where p is read anyway —
+//           one vector pass less per iteration; x is still updated before
+//           the loop can stop); every CTA derives ||r||, convergence / limit
+//           (pcg.cpp:90-99) and beta = rho' / rho from red[1..2]; unless
+//           stopping, p = r/d + beta p and Ap = (constrained & owned ? p : 0),
+//           the next RED target; the last CTA records the iteration (or the
+//           stop) and red[3] = sum of p^2 over owned constrained rows
 // On a partitioned problem red[] is all-reduced across ranks between the
 // kernels (dist.cu); on one GPU the same kernels run back to back.  Each
 // reduction is per-CTA partials over a fixed grid summed in a fixed order by
@@ -124,8 +126,8 @@ __global__ void pcg_init_finalize(PcgState* st, double* hist) {
 template <bool VEC, bool OWN>
 __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
     pcg_update_kernel(PcgState* st, int it, int64_t n_L, int m, const double* __restrict__ d,
-                      double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                      const double* __restrict__ Ap, const uint32_t* own, double* part, int rev) {
+                      double* __restrict__ r, const double* __restrict__ Ap, const uint32_t* own,
+                      double* part, int rev) {
   __shared__ double scratch[VT / 32];
   pdl_wait();
   if (st->stop) return;
@@ -153,19 +155,14 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
     const int64_t o = c * n_L;
     if constexpr (VEC) {
       const int64_t h = n_L / 2;
-      double2* x2 = reinterpret_cast<double2*>(x + o);
       double2* r2 = reinterpret_cast<double2*>(r + o);
-      const double2* p2 = reinterpret_cast<const double2*>(p + o);
       const double2* a2 = reinterpret_cast<const double2*>(Ap + o);
       const double2* d2 = reinterpret_cast<const double2*>(d + o);
       const double2 one2 = make_double2(1.0, 1.0);
-      auto two = [&](int64_t k, double2 xv, double2 pv, double2 rv, double2 av, double2 dv) {
+      auto two = [&](int64_t k, double2 rv, double2 av, double2 dv) {
         // (k is already the swept pair index)
-        xv.x += alpha * pv.x;
-        xv.y += alpha * pv.y;
         rv.x -= alpha * av.x;
         rv.y -= alpha * av.y;
-        x2[k] = xv;
         r2[k] = rv;
         const int64_t node = 2 * k;
         if constexpr (OWN) {
@@ -181,20 +178,19 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
       int64_t j = tid;
       for (; j + stride < h; j += 2 * stride) {
         const int64_t k = rev ? h - 1 - j : j, k1 = rev ? k - stride : k + stride;
-        const double2 xa = x2[k], pa = p2[k], ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
-        const double2 xb = x2[k1], pb = p2[k1], rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
-        two(k, xa, pa, ra, aa, da);
-        two(k1, xb, pb, rb, ab, db);
+        const double2 ra = r2[k], aa = a2[k], da = d ? d2[k] : one2;
+        const double2 rb = r2[k1], ab = a2[k1], db = d ? d2[k1] : one2;
+        two(k, ra, aa, da);
+        two(k1, rb, ab, db);
       }
       if (j < h) {
         const int64_t k = rev ? h - 1 - j : j;
-        two(k, x2[k], p2[k], r2[k], a2[k], d ? d2[k] : one2);
+        two(k, r2[k], a2[k], d ? d2[k] : one2);
       }
     } else {
       for (int64_t jn = tid; jn < n_L; jn += stride) {
         const int64_t node = rev ? n_L - 1 - jn : jn;
         const int64_t i = o + node;
-        x[i] += alpha * p[i];
         const double ri = r[i] - alpha * Ap[i];
         r[i] = ri;
         const double w = OWN ? owned_w(own, node) : 1.0;
@@ -228,31 +224,20 @@ template <bool VEC>
 __global__ void __launch_bounds__(VT, 4)
     pcg_direction_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                          const double* __restrict__ d, const double* __restrict__ r,
-                         double* __restrict__ p, double* __restrict__ Ap,
+                         double* __restrict__ x, double* __restrict__ p, double* __restrict__ Ap,
                          const uint32_t* cons_mask, const uint32_t* own, double* part, int rev) {
   __shared__ double scratch[VT / 32];
   pdl_wait();
-  if (st->stop) return;
+  if (st->stop) return;  // stopped by the update kernel (pAp check): x untouched
+  const double alpha = st->alpha;
   const double rr = st->red[1], rz = st->red[2];
   const double res = sqrt(rr);
   const double rho = st->rho;
   const bool bad = !isfinite(res);
   const bool conv = res <= st->target;
+  // stopping: only x += alpha p below; the last CTA publishes the stop (no
+  // CTA may see st->stop set before it has done its part of x)
   const bool stop = bad || (conv && !st->fixed) || it == st->limit || res == 0.0;
-  if (stop) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (bad) {
-        st->error = PCG_ERR_RESID;
-      } else {
-        st->it = it;
-        st->res = res;
-        hist[it] = res;
-        if (conv) st->converged = 1;
-      }
-      st->stop = 1;
-    }
-    return;
-  }
   const double beta = rz / rho;
   double cc = 0.0;
   const int64_t tid = (int64_t)blockIdx.x * VT + threadIdx.x;
@@ -265,7 +250,12 @@ __global__ void __launch_bounds__(VT, 4)
       const double2* d2 = reinterpret_cast<const double2*>(d + o);
       double2* p2 = reinterpret_cast<double2*>(p + o);
       double2* a2 = reinterpret_cast<double2*>(Ap + o);
-      auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv) {
+      double2* x2 = reinterpret_cast<double2*>(x + o);
+      auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv, double2 xv) {
+        xv.x += alpha * pv.x;
+        xv.y += alpha * pv.y;
+        x2[k] = xv;
+        if (stop) return;
         double2 q;
         q.x = rv.x * dv.x + beta * pv.x;  // dv = 1/diag (or 1)
         q.y = rv.y * dv.y + beta * pv.y;
@@ -281,21 +271,26 @@ __global__ void __launch_bounds__(VT, 4)
       int64_t j = tid;
       for (; j + stride < h; j += 2 * stride) {
         const int64_t k = rev ? h - 1 - j : j, k1 = rev ? k - stride : k + stride;
-        const double2 ra = r2[k], pa = p2[k], da = d ? d2[k] : one2;
-        const double2 rb = r2[k1], pb = p2[k1], db = d ? d2[k1] : one2;
-        two(k, ra, pa, da);
-        two(k1, rb, pb, db);
+        const double2 pa = p2[k], xa = x2[k];
+        const double2 pb = p2[k1], xb = x2[k1];
+        const double2 ra = stop ? one2 : r2[k], da = (d && !stop) ? d2[k] : one2;
+        const double2 rb = stop ? one2 : r2[k1], db = (d && !stop) ? d2[k1] : one2;
+        two(k, ra, pa, da, xa);
+        two(k1, rb, pb, db, xb);
       }
       if (j < h) {
         const int64_t k = rev ? h - 1 - j : j;
-        two(k, r2[k], p2[k], d ? d2[k] : one2);
+        two(k, stop ? one2 : r2[k], p2[k], (d && !stop) ? d2[k] : one2, x2[k]);
       }
     } else {
       for (int64_t jn = tid; jn < n_L; jn += stride) {
         const int64_t node = rev ? n_L - 1 - jn : jn;
         const int64_t i = o + node;
+        const double po = p[i];
+        x[i] += alpha * po;
+        if (stop) continue;
         const double zi = d ? r[i] * d[i] : r[i];  // d holds 1/diag here
-        const double pi = zi + beta * p[i];
+        const double pi = zi + beta * po;
         const bool cw = is_cons(cons_mask, node) && owned_w(own, node) != 0.0;
         p[i] = pi;
         Ap[i] = cw ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
@@ -309,6 +304,18 @@ __global__ void __launch_bounds__(VT, 4)
   const double tc = pcg_sum_partials<VT>(part, gridDim.x, scratch);
   if (threadIdx.x == 0) {
     st->counter[2] = 0;
+    if (stop) {
+      if (bad) {
+        st->error = PCG_ERR_RESID;
+      } else {
+        st->it = it;
+        st->res = res;
+        hist[it] = res;
+        if (conv) st->converged = 1;
+      }
+      st->stop = 1;
+      return;
+    }
     st->red[3] = tc;
     st->it = it;
     st->res = res;
@@ -363,25 +370,26 @@ cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist)
 }
 
 cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
-                              const double* d, double* x, double* r, const double* p,
-                              const double* Ap, const uint32_t* own, double* part, int rev) {
-  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(x) && aligned16(r) &&
-                   aligned16(p) && aligned16(Ap);
+                              const double* d, double* r, const double* Ap, const uint32_t* own,
+                              double* part, int rev) {
+  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(Ap);
   auto k = vec ? (own ? pcg_update_kernel<true, true> : pcg_update_kernel<true, false>)
                : (own ? pcg_update_kernel<false, true> : pcg_update_kernel<false, false>);
   const cudaError_t err =
-      launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, n_L, m, d, x, r, p, Ap, own, part, rev);
+      launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, n_L, m, d, r, Ap, own, part, rev);
   count_launch();
   return err;
 }
 
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
-                                 int m, const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, const uint32_t* own, double* part, int rev) {
-  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(p) && aligned16(Ap);
+                                 int m, const double* d, const double* r, double* x, double* p,
+                                 double* Ap, const uint32_t* mask, const uint32_t* own, double* part,
+                                 int rev) {
+  const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(x) &&
+                   aligned16(p) && aligned16(Ap);
   auto k = vec ? pcg_direction_kernel<true> : pcg_direction_kernel<false>;
   const cudaError_t err = launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, hist, n_L, m, d,
-                                     r, p, Ap, mask, own, part, rev);
+                                     r, x, p, Ap, mask, own, part, rev);
   count_launch();
   return err;
 }

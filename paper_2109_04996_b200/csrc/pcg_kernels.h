@@ -15,11 +15,11 @@ cudaError_t pcg_launch_init(cudaStream_t s, PcgState* st, int64_t n_L, int m, co
                             double* Ap, const uint32_t* mask, const uint32_t* own, double* part);
 cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist);
 cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
-                              const double* d, double* x, double* r, const double* p,
-                              const double* Ap, const uint32_t* own, double* part, int rev = 0);
+                              const double* d, double* r, const double* Ap, const uint32_t* own,
+                              double* part, int rev = 0);
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
-                                 int m, const double* d, const double* r, double* p, double* Ap,
-                                 const uint32_t* mask, const uint32_t* own, double* part,
-                                 int rev = 0);
+                                 int m, const double* d, const double* r, double* x, double* p,
+                                 double* Ap, const uint32_t* mask, const uint32_t* own,
+                                 double* part, int rev = 0);
 
 }  // namespace hxf
