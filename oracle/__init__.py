@@ -89,6 +89,8 @@ def _lib(impl: str) -> C.CDLL:
     L.orc_apply_basis.argtypes = [I, I, I, I, I, I64, pd, I64, pd, I64]
     if impl == "reference":
         L.orc_run_bench.argtypes = [I, I, I, I, I, I, I, I, pd]
+        L.orc_sweep_model.argtypes = [I, I, pi, I, pi, I, I, D, D, C.c_char_p, I64, pd]
+        L.orc_record_json.argtypes = [C.c_char_p, I, I, I64, I64, I, I, D, D, D, C.c_char_p, I64]
     _LIBS[impl] = L
     return L
 
@@ -337,3 +339,28 @@ class RefWithBackend:
             self._L.orh_free(self._h)
         except Exception:
             pass
+
+
+def sweep_model_reference(bp: str, p: int, dims_list, threads, iters: int, a: float, b: float):
+    """The reference's run_scaling_sweep + sweep_csv under its own synthetic
+    timing model (tests/test_bench.cpp:142-150): (csv text, r_max, n08|None, C)."""
+    L = _lib("reference")
+    dims = np.ascontiguousarray(np.asarray(dims_list, dtype=np.int32).reshape(-1))
+    thr = np.ascontiguousarray(np.asarray(threads, dtype=np.int32))
+    buf = C.create_string_buffer(1 << 20)
+    summ = np.zeros(3)
+    _check(L, L.orc_sweep_model(int(bp[2]), p, dims.ctypes.data_as(C.POINTER(C.c_int)), len(dims_list),
+                                thr.ctypes.data_as(C.POINTER(C.c_int)), len(threads), iters, a, b,
+                                buf, len(buf), _dp(summ)))
+    n08 = None if summ[1] < 0 else float(summ[1])
+    return buf.value.decode(), float(summ[0]), n08, float(summ[2])
+
+
+def record_json_reference(rec: dict) -> str:
+    """The reference's bench_record_json (nlohmann::ordered_json dump)."""
+    L = _lib("reference")
+    buf = C.create_string_buffer(4096)
+    _check(L, L.orc_record_json(rec["bp"].encode(), rec["p"], rec["q"], rec["E"], rec["n"], rec["P"],
+                                rec["iterations"], rec["seconds"], rec["dofs_rate"], rec["n_per_rank"],
+                                buf, len(buf)))
+    return buf.value.decode()

@@ -16,6 +16,10 @@
 //   orc_basis      -> hexfem::make_basis          (proj/src/tensor_basis.cpp:40-71)
 //   orc_apply_basis-> hexfem::apply_basis_batch   (proj/src/contraction.cpp:248-332)
 //   orc_run_bench  -> hexfem::run_bench           (proj/src/bench.cpp:191-229)
+//   orc_sweep_model-> hexfem::run_scaling_sweep + sweep_csv with the synthetic
+//                     timing model of tests/test_bench.cpp:142-150
+//   orc_record_json-> hexfem::bench_record_json   (proj/src/bench.cpp:351-363)
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -216,6 +220,48 @@ int orc_run_bench(int bp, int p, int nx, int ny, int nz, int deform, int threads
     rec[3] = double(r.E);
     rec[4] = r.q;
     rec[5] = r.dofs_rate;
+  });
+}
+
+// Scaling sweep under the timing model T(n,1) = a n, T(n,P>1) = a n / P + b
+// (the reference's own test model): writes sweep_csv() into csv (NUL-terminated,
+// cap bytes) and summary = {r_max, n08 (or -1), work_constant}.
+int orc_sweep_model(int bp, int p, const int* dims, int ndims, const int* threads, int nthreads,
+                    int iters, double a, double b, char* csv, int64_t cap, double* summary) {
+  return guarded([&] {
+    std::vector<std::array<int, 3>> dl;
+    for (int i = 0; i < ndims; ++i) dl.push_back({dims[3 * i], dims[3 * i + 1], dims[3 * i + 2]});
+    std::vector<int> tl(threads, threads + nthreads);
+    const TimingModel model = [&](std::int64_t n, int P) {
+      return P == 1 ? a * double(n) : a * double(n) / P + b;
+    };
+    const auto res = run_scaling_sweep(BpId(bp), p, dl, tl, iters, Deformation::None, model);
+    const std::string text = sweep_csv(res);
+    if (int64_t(text.size()) + 1 > cap) throw std::invalid_argument("orc_sweep_model: buffer");
+    std::memcpy(csv, text.c_str(), text.size() + 1);
+    summary[0] = res.summary.r_max;
+    summary[1] = res.summary.n08_per_rank ? *res.summary.n08_per_rank : -1.0;
+    summary[2] = res.summary.work_constant;
+  });
+}
+
+int orc_record_json(const char* bp, int p, int q, int64_t E, int64_t n, int P, int iters,
+                    double seconds, double dofs_rate, double n_per_rank, char* out, int64_t cap) {
+  return guarded([&] {
+    BenchRecord r;
+    r.bp = bp;
+    r.p = p;
+    r.q = q;
+    r.E = E;
+    r.n = n;
+    r.P = P;
+    r.iterations = iters;
+    r.seconds = seconds;
+    r.dofs_rate = dofs_rate;
+    r.n_per_rank = n_per_rank;
+    const std::string text = bench_record_json(r);
+    if (int64_t(text.size()) + 1 > cap) throw std::invalid_argument("orc_record_json: buffer");
+    std::memcpy(out, text.c_str(), text.size() + 1);
   });
 }
 

@@ -8,6 +8,7 @@
 #include "hexfem_b200.hpp"
 
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -699,6 +700,150 @@ BenchRecord run_bench(const BpConfig& config) {
   rec.n_per_rank = double(rec.n) / rec.P;
   rec.apply_seconds = apply_s;
   return rec;
+}
+
+// ---------------------------------------------------------------- sweeps
+// (bench.cpp:231-330: the same grouping, ordering and efficiency algebra)
+SweepResult run_scaling_sweep(BpId bp, int p, const std::vector<std::array<int, 3>>& dims_list,
+                              const std::vector<int>& ranks_list, int iterations,
+                              Deformation deformation, const TimingModel& timing_override) {
+  if (std::find(ranks_list.begin(), ranks_list.end(), 1) == ranks_list.end())
+    throw std::invalid_argument("run_scaling_sweep: threads list must include 1");
+  if (!timing_override)
+    for (const int P : ranks_list)
+      if (P != 1)
+        throw std::invalid_argument(
+            "run_scaling_sweep: measuring P > 1 needs one process per GPU "
+            "(bench.py --gpus P); pass a timing model for P > 1");
+  SweepResult out;
+  for (const auto& dims : dims_list) {
+    std::vector<BenchRecord> group;
+    for (const int P : ranks_list) {
+      BenchRecord rec;
+      if (timing_override) {
+        rec.bp = bp_name(bp);
+        rec.p = p;
+        rec.q = bp_quadrature_points(bp, p);
+        rec.E = int64_t(dims[0]) * dims[1] * dims[2];
+        rec.n = bp_dof_count(bp, p, dims);
+        rec.P = P;
+        rec.iterations = iterations;
+        rec.seconds = timing_override(rec.n, P);
+        rec.dofs_rate = double(rec.n) * rec.iterations / rec.seconds;
+        rec.n_per_rank = double(rec.n) / rec.P;
+      } else {
+        BpConfig c;
+        c.bp = bp;
+        c.p = p;
+        c.dims = dims;
+        c.deformation = deformation;
+        c.fixed_iterations = iterations;
+        rec = run_bench(c);
+      }
+      group.push_back(rec);
+    }
+    double t1 = 0;
+    for (const auto& r : group)
+      if (r.P == 1) t1 = r.seconds;
+    for (auto& r : group) {
+      ScalingRow row;
+      row.T_1 = t1;
+      row.T_P = r.seconds;
+      row.eta = t1 / (r.P * r.seconds);
+      row.record = std::move(r);
+      out.rows.push_back(std::move(row));
+    }
+  }
+  out.summary = scaling_summary(out.rows);
+  return out;
+}
+
+ScalingSummary scaling_summary(std::vector<ScalingRow>& rows) {
+  std::sort(rows.begin(), rows.end(), [](const ScalingRow& a, const ScalingRow& b) {
+    if (a.record.n_per_rank != b.record.n_per_rank) return a.record.n_per_rank < b.record.n_per_rank;
+    if (a.record.n != b.record.n) return a.record.n < b.record.n;
+    return a.record.P < b.record.P;
+  });
+  ScalingSummary s;
+  for (const auto& r : rows) s.r_max = std::max(s.r_max, r.record.dofs_rate / r.record.P);
+  // first upward crossing of eta = 0.8 among the P > 1 rows (P = 1 has eta 1)
+  const ScalingRow* prev = nullptr;
+  for (const auto& r : rows) {
+    if (r.record.P <= 1) continue;
+    if (prev && prev->eta < 0.8 && r.eta >= 0.8) {
+      const double x0 = std::log(prev->record.n_per_rank), x1 = std::log(r.record.n_per_rank);
+      const double t = (0.8 - prev->eta) / (r.eta - prev->eta);
+      s.n08_per_rank = std::exp(x0 + t * (x1 - x0));
+      break;
+    }
+    prev = &r;
+  }
+  double num = 0, den = 0;
+  if (s.r_max > 0)
+    for (const auto& r : rows) {
+      const double xi = double(r.record.n) / (r.eta * r.record.P * s.r_max);
+      num += r.T_P * xi;
+      den += xi * xi;
+    }
+  s.work_constant = den > 0 ? num / den : 0.0;
+  return s;
+}
+
+double time_to_solution(double work_constant, double n, double eta, double P, double r_max) {
+  return work_constant * n / (eta * P * r_max);
+}
+
+std::string format_double(double v) {
+  char buf[64];
+  const auto res = std::to_chars(buf, buf + sizeof buf, v);
+  return std::string(buf, res.ptr);
+}
+
+namespace {
+std::string json_double(double v) {  // JSON number, round-trip exact
+  if (!std::isfinite(v)) return "null";
+  std::string s = format_double(v);
+  if (s.find_first_of(".eE") == std::string::npos) s += ".0";
+  return s;
+}
+std::string json_string(const std::string& v) {
+  std::string o = "\"";
+  for (const char c : v) {
+    if (c == '"' || c == '\\') o += '\\';
+    o += c;
+  }
+  return o + "\"";
+}
+std::string csv_field(const std::string& v) {
+  if (v.find_first_of(",\"\r\n") == std::string::npos) return v;
+  std::string o = "\"";
+  for (const char c : v) o += (c == '"') ? std::string("\"\"") : std::string(1, c);
+  return o + "\"";
+}
+}  // namespace
+
+std::string bench_record_json(const BenchRecord& r) {
+  return "{\"bp\":" + json_string(r.bp) + ",\"p\":" + std::to_string(r.p) +
+         ",\"q\":" + std::to_string(r.q) + ",\"E\":" + std::to_string(r.E) +
+         ",\"n\":" + std::to_string(r.n) + ",\"P\":" + std::to_string(r.P) +
+         ",\"iterations\":" + std::to_string(r.iterations) + ",\"seconds\":" +
+         json_double(r.seconds) + ",\"dofs_rate\":" + json_double(r.dofs_rate) +
+         ",\"n_per_rank\":" + json_double(r.n_per_rank) + "}";
+}
+
+std::string sweep_csv_header() { return "bp,p,q,E,n,P,iters,seconds,dofs_rate,n_per_rank,eta"; }
+
+std::string sweep_csv(const SweepResult& result) {
+  std::string o = sweep_csv_header() + "\n";
+  for (const auto& row : result.rows) {
+    const BenchRecord& r = row.record;
+    o += csv_field(r.bp) + "," + std::to_string(r.p) + "," + std::to_string(r.q) + "," +
+         std::to_string(r.E) + "," + std::to_string(r.n) + "," + std::to_string(r.P) + "," +
+         std::to_string(r.iterations) + "," + format_double(r.seconds) + "," +
+         format_double(r.dofs_rate) + "," + format_double(r.n_per_rank) + "," +
+         format_double(row.eta) + "\n";
+  }
+  return o;
 }
 
 std::vector<double> assemble_dense(BpProblem& problem) {

@@ -248,6 +248,39 @@ struct BenchRecord {
 };
 BenchRecord run_bench(const BpConfig& config);
 
+// Scaling sweeps and record formats (bench.hpp:97-140, bench.cpp:231-381).  P
+// is the rank (GPU) count here — the reference's worker-thread count.
+struct ScalingRow {
+  BenchRecord record;
+  double T_1 = 0;  // seconds at P = 1, same problem
+  double T_P = 0;
+  double eta = 0;  // T_1 / (P T_P)
+};
+struct ScalingSummary {
+  double r_max = 0;                     // max dofs_rate per rank
+  std::optional<double> n08_per_rank;   // n/P where eta crosses 0.8 (log-linear)
+  double work_constant = 0;             // C of t = C n / (eta P r_max), least squares
+};
+struct SweepResult {
+  std::vector<ScalingRow> rows;  // ascending n/P, then n, then P
+  ScalingSummary summary;
+};
+using TimingModel = std::function<double(int64_t n, int P)>;
+
+// Measured mode runs P = 1 on this process's GPU; P > 1 needs one process per
+// GPU (bench.py --gpus P) and is rejected here unless a timing model is given.
+SweepResult run_scaling_sweep(BpId bp, int p, const std::vector<std::array<int, 3>>& dims_list,
+                              const std::vector<int>& ranks_list, int iterations,
+                              Deformation deformation = Deformation::None,
+                              const TimingModel& timing_override = {});
+// rows -> summary (also usable on records gathered from separate bench runs)
+ScalingSummary scaling_summary(std::vector<ScalingRow>& rows);
+double time_to_solution(double work_constant, double n, double eta, double P, double r_max);
+std::string format_double(double v);  // shortest round-trip form
+std::string bench_record_json(const BenchRecord& rec);
+std::string sweep_csv_header();
+std::string sweep_csv(const SweepResult& result);
+
 // Dense matrix of the operator by applying it to unit vectors on the device
 // (the reference's reference_assemble is a dense quadrature loop, oracle only;
 // operator.cpp:258-349).  Rejected above 20000 unknowns like the reference.

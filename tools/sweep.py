@@ -4,6 +4,11 @@ roofline fraction of each (algorithmic bytes / time / measured HBM peak).
 
 Usage: python tools/sweep.py [--bp bp5] [--p 1-15] [--sizes 1e5,1e6,1e7]
        [--deform sine] [--out profiles/r1_sweep_bp5.md]
+       [--records sweep.jsonl] [--csv sweep.csv]
+--records writes one reference BenchRecord JSON per point (bench.cpp:351-363,
+P = 1 GPU) and --csv the reference's sweep CSV (bench.cpp:365-381, eta = 1 at
+P = 1; multi-GPU rows come from bench.py --gpus N and
+_core.scaling_summary).
 Elements per axis come from SURVEY §8(d)'s C5 table: d chosen so that
 n = m (d p - 1)^3 is closest to the target (constrained BPs)."""
 import argparse
@@ -64,6 +69,8 @@ def main():
     ap.add_argument("--deform", default="sine")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--records", default=None)
+    ap.add_argument("--csv", default=None)
     a = ap.parse_args()
     peak = json.load(open(ROOT / "MEASURED_PEAKS.json"))["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     rows = []
@@ -108,10 +115,23 @@ def main():
                        k1_us=k1 * 1e6, k1_frac=bapply / k1 / 1e9 / peak,
                        cg_us=t_it * 1e6, cg_gdofs=n / t_it / 1e9,
                        cg_frac=bcg / t_it / 1e9 / peak, setup_s=tsetup)
+            q = p + 2 if int(a.bp[2]) <= 4 else p + 1
+            row["record"] = dict(bp=a.bp, p=p, q=q, E=d ** 3, n=n, P=1, iterations=a.iters,
+                                 seconds=best, dofs_rate=n * a.iters / best, n_per_rank=float(n))
             rows.append(row)
-            print(json.dumps(row), flush=True)
+            print(json.dumps({k: v for k, v in row.items() if k != "record"}), flush=True)
             del prob, x, y, xs
             torch.cuda.empty_cache()
+    from paper_2109_04996_b200 import _core
+    if a.records:
+        with open(a.records, "w") as f:
+            for r in rows:
+                f.write(_core.bench_record_json(r["record"]) + "\n")
+    if a.csv:
+        srows = [dict(record=r["record"], T_1=r["record"]["seconds"], T_P=r["record"]["seconds"],
+                      eta=1.0) for r in rows]
+        with open(a.csv, "w") as f:
+            f.write(_core.scaling_summary(srows)["csv"])
     if a.out:
         with open(a.out, "w") as f:
             f.write(f"# {a.bp} throughput sweep ({a.deform} box, {a.iters} fixed CG iterations, "
