@@ -1,5 +1,6 @@
 // Instantiates the fused operator kernel for one degree P = p+1 (included by
 // op_inst_p<P>.cu with HXF_P defined, so the instances compile in parallel).
+#include <cmath>
 #include <cstring>
 
 #include "op_kernel.cuh"
@@ -44,6 +45,25 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
   kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
   count_launch();
   return cudaGetLastError();
+}
+
+// The line kernel's even-odd contractions need centro-symmetric 1-D matrices
+// (B[q-1-i][p-j] = B[i][j], D[q-1-i][q-1-j] = -D[i][j]: symmetric GLL nodes and
+// Gauss / GLL points, make_basis, tensor_basis.cpp:40-71).  Anything else
+// takes the general kernel.
+inline bool centro_symmetric(int P, int Q, bool interp, const double* B, const double* D) {
+  auto close = [](double a, double b, double scale) { return std::fabs(a - b) <= 1e-13 * scale; };
+  double sb = 0, sd = 0;
+  for (int i = 0; i < Q * P; ++i) sb = std::fmax(sb, std::fabs(B[i]));
+  for (int i = 0; i < Q * Q; ++i) sd = std::fmax(sd, std::fabs(D[i]));
+  for (int o = 0; o < Q; ++o)
+    for (int a = 0; a < Q; ++a)
+      if (!close(D[(Q - 1 - o) * Q + (Q - 1 - a)], -D[o * Q + a], sd)) return false;
+  if (interp)
+    for (int o = 0; o < Q; ++o)
+      for (int a = 0; a < P; ++a)
+        if (!close(B[(Q - 1 - o) * P + (P - 1 - a)], B[o * P + a], sb)) return false;
+  return true;
 }
 
 // Line kernel (op_line.cuh): interpolating bases and the large collocated sizes.
@@ -183,7 +203,7 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
     if (qk == 1 && NC == 3 && use_pencil<P, 3>() && !pencil_disabled())
       return run_pencil_gm<P, 3>(prm, D, s, g);
   }
-  if (op_kernel_choice() != 2) {
+  if (op_kernel_choice() != 2 && centro_symmetric(P, Q, INTERP, B, D)) {
     if (NC == 1 && qk == 1) return run_line<LineTraits<P, Q, 1, 1, INTERP>>(prm, B, D, s, g);
     if (NC == 1 && qk == 2) return run_line<LineTraits<P, Q, 1, 2, INTERP>>(prm, B, D, s, g);
     if (NC == 3 && qk == 1) return run_line<LineTraits<P, Q, 3, 1, INTERP>>(prm, B, D, s, g);

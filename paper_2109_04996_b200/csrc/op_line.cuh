@@ -57,10 +57,18 @@ struct LineTraits {
   static constexpr int NQD = DIFF ? 6 : 1;
   static constexpr int QDS = round_up(NQD * Q3, 2);  // padded doubles per element
   // 1-D matrices in shared memory, 16-byte rows (broadcast LDS.128 row loads):
-  // B [Q][RP], B^T [P][RQ], D [Q][RQ], D^T [Q][RQ]
-  static constexpr int RP = round_up(P, 2), RQ = round_up(Q, 2);
-  static constexpr int OFF_B = 0, OFF_BT = Q * RP, OFF_D = OFF_BT + P * RQ, OFF_DT = OFF_D + Q * RQ;
-  static constexpr int OFF_S = round_up(OFF_DT + Q * RQ, 2);
+  // D [Q][RQ] (late z-derivative form) and the even-odd tables below
+  static constexpr int RQ = round_up(Q, 2);
+  static constexpr int OFF_D = 0;
+  // even-odd tables (centro-symmetric bases: M[NO-1-o][NI-1-a] = +-M[o][a]):
+  // row o < ceil(NO/2) = [ (M[o][a] + M[o][a'])/2 (a < NI/2) | M[o][NI/2] (odd NI)
+  // | (M[o][a] - M[o][a'])/2 ], a' = NI-1-a, for B, B^T, D, D^T
+  __host__ __device__ static constexpr int eo_rt(int ni) { return round_up(2 * (ni / 2) + 1, 2); }
+  static constexpr int OFF_EBF = round_up(OFF_D + Q * RQ, 2);           // B   (Q x P)
+  static constexpr int OFF_EBT = OFF_EBF + ((Q + 1) / 2) * eo_rt(P);    // B^T (P x Q)
+  static constexpr int OFF_EDF = OFF_EBT + ((P + 1) / 2) * eo_rt(Q);    // D   (Q x Q)
+  static constexpr int OFF_EDT = OFF_EDF + ((Q + 1) / 2) * eo_rt(Q);    // D^T (Q x Q)
+  static constexpr int OFF_S = round_up(OFF_EDT + ((Q + 1) / 2) * eo_rt(Q), 2);
   static constexpr int SMEM_BYTES = (OFF_S + EPB * 3 * SLAB) * 8;
   __device__ static __forceinline__ int off(int k, int j, int i) { return (k * Q + j) * RS + i; }
 };
@@ -131,6 +139,35 @@ __device__ __forceinline__ void lc(const double* colm, int cstr, const double* r
     line_contract<NI, NO>(colm, cstr, in, out);
 }
 
+// Even-odd ("centro-symmetric") contraction: out[o] = sum_a M[o][a] in[a] for a
+// NO x NI matrix with M[NO-1-o][NI-1-a] = S M[o][a] (S = +1 interpolation,
+// -1 derivative on symmetric GLL / Gauss points), from the half-size table of
+// LineTraits (one row per output pair): half the multiply-adds and row loads.
+template <int NI, int NO, int S>
+__device__ __forceinline__ void eo_contract(const double* tab, const double* in, double* out) {
+  constexpr int HI = NI / 2, HO = (NO + 1) / 2, L = 2 * HI + 1, RT = (L + 1) / 2 * 2;
+  double e[HI > 0 ? HI : 1], f[HI > 0 ? HI : 1];
+#pragma unroll
+  for (int a = 0; a < HI; ++a) {
+    e[a] = in[a] + in[NI - 1 - a];
+    f[a] = in[a] - in[NI - 1 - a];
+  }
+#pragma unroll
+  for (int o = 0; o < HO; ++o) {
+    double row[L];
+    line_row<L>(tab + o * RT, row);
+    double E = 0.0, F = 0.0;
+#pragma unroll
+    for (int a = 0; a < HI; ++a) {
+      E += row[a] * e[a];
+      F += row[HI + 1 + a] * f[a];
+    }
+    if constexpr (NI & 1) E += row[HI] * in[HI];
+    out[o] = E + F;
+    if (NO - 1 - o != o) out[NO - 1 - o] = S > 0 ? E - F : F - E;
+  }
+}
+
 // a contiguous slab line (x-line) to / from registers
 template <int N>
 __device__ __forceinline__ void ld_line(const double* src, double* d) {
@@ -148,27 +185,46 @@ __device__ __forceinline__ void st_line(double* dst, const double* d) {
 // feeding both lines; results to the same lines of dx / dy (in place safe:
 // both lines are read before the first write).
 template <class T>
-__device__ __forceinline__ void line_pair(const double* m, const double* sx, const double* sy,
+__device__ __forceinline__ void line_pair(const double* tab, const double* sx, const double* sy,
                                           double* dx, double* dy, int a, int b) {
-  constexpr int Q = T::Q;
-  double lx[Q], ly[Q];
+  // tab: even-odd table of a Q x Q derivative matrix (S = -1)
+  constexpr int Q = T::Q, HI = Q / 2, HO = (Q + 1) / 2, L = 2 * HI + 1, RT = (L + 1) / 2 * 2;
+  double ex[HI], fx[HI], ey[HI], fy[HI], mx = 0.0, my = 0.0;
 #pragma unroll
-  for (int i = 0; i < Q; ++i) {
-    lx[i] = sx[T::off(b, a, i)];
-    ly[i] = sy[T::off(b, i, a)];
+  for (int i = 0; i < HI; ++i) {
+    const double x0 = sx[T::off(b, a, i)], x1 = sx[T::off(b, a, Q - 1 - i)];
+    const double y0 = sy[T::off(b, i, a)], y1 = sy[T::off(b, Q - 1 - i, a)];
+    ex[i] = x0 + x1;
+    fx[i] = x0 - x1;
+    ey[i] = y0 + y1;
+    fy[i] = y0 - y1;
+  }
+  if constexpr (Q & 1) {
+    mx = sx[T::off(b, a, HI)];
+    my = sy[T::off(b, HI, a)];
   }
 #pragma unroll
-  for (int o = 0; o < Q; ++o) {
-    double row[Q];
-    line_row<Q>(m + o * T::RQ, row);
-    double px = 0.0, py = 0.0;
+  for (int o = 0; o < HO; ++o) {
+    double row[L];
+    line_row<L>(tab + o * RT, row);  // one row feeds both lines
+    double Ex = 0.0, Fx = 0.0, Ey = 0.0, Fy = 0.0;
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-      px += row[i] * lx[i];
-      py += row[i] * ly[i];
+    for (int i = 0; i < HI; ++i) {
+      Ex += row[i] * ex[i];
+      Fx += row[HI + 1 + i] * fx[i];
+      Ey += row[i] * ey[i];
+      Fy += row[HI + 1 + i] * fy[i];
     }
-    dx[T::off(b, a, o)] = px;
-    dy[T::off(b, o, a)] = py;
+    if constexpr (Q & 1) {
+      Ex += row[HI] * mx;
+      Ey += row[HI] * my;
+    }
+    dx[T::off(b, a, o)] = Ex + Fx;
+    dy[T::off(b, o, a)] = Ey + Fy;
+    if (Q - 1 - o != o) {
+      dx[T::off(b, a, Q - 1 - o)] = Fx - Ex;
+      dy[T::off(b, Q - 1 - o, a)] = Fy - Ey;
+    }
   }
 }
 
@@ -186,22 +242,30 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   const int l = tid - slot * QQ;
   const bool aslot = slot < EPB;
   double* S0 = smem + T::OFF_S + (aslot ? slot : 0) * 3 * T::SLAB;
-  const double* sB = smem + T::OFF_B;
-  const double* sBT = smem + T::OFF_BT;
   const double* sD = smem + T::OFF_D;
-  const double* sDT = smem + T::OFF_DT;
-  for (int t = tid; t < Q * Q; t += NT) {
-    const int r = t / Q, c = t % Q;
-    smem[T::OFF_D + r * T::RQ + c] = mats.D[t];
-    smem[T::OFF_DT + c * T::RQ + r] = mats.D[t];
-  }
-  if constexpr (T::INTERP) {
-    for (int t = tid; t < Q * P; t += NT) {
-      const int r = t / P, c = t % P;  // B[r][c]
-      smem[T::OFF_B + r * T::RP + c] = mats.B[t];
-      smem[T::OFF_BT + c * T::RQ + r] = mats.B[t];
+  const double* eBF = smem + T::OFF_EBF;
+  const double* eBT = smem + T::OFF_EBT;
+  const double* eDF = smem + T::OFF_EDF;
+  const double* eDT = smem + T::OFF_EDT;
+  for (int t = tid; t < Q * Q; t += NT) smem[T::OFF_D + (t / Q) * T::RQ + t % Q] = mats.D[t];
+  // even-odd tables from the full matrices (M(o, a) accessors)
+  auto eo_table = [&](int off, int NO, int NI, auto M) {
+    const int HI = NI / 2, RT = T::eo_rt(NI), HO = (NO + 1) / 2;
+    for (int t = tid; t < HO * RT; t += NT) {
+      const int o = t / RT, c = t % RT;
+      double v = 0.0;
+      if (c < HI) v = 0.5 * (M(o, c) + M(o, NI - 1 - c));
+      else if (c == HI) v = (NI & 1) ? M(o, HI) : 0.0;
+      else if (c < 2 * HI + 1) v = 0.5 * (M(o, c - HI - 1) - M(o, NI - 1 - (c - HI - 1)));
+      smem[off + t] = v;
     }
+  };
+  if constexpr (T::INTERP) {
+    eo_table(T::OFF_EBF, Q, P, [&](int o, int a) { return mats.B[o * P + a]; });
+    eo_table(T::OFF_EBT, P, Q, [&](int o, int a) { return mats.B[a * P + o]; });
   }
+  eo_table(T::OFF_EDF, Q, Q, [&](int o, int a) { return mats.D[o * Q + a]; });
+  eo_table(T::OFF_EDT, Q, Q, [&](int o, int a) { return mats.D[a * Q + o]; });
   __syncthreads();
   double* S1 = S0 + T::SLAB;
   double* S2 = S1 + T::SLAB;
@@ -308,7 +372,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         // ---- 1: x-interp of the gathered x-line -> S0 [k][j][qi] ----
         if (gthread) {
           double t[Q];
-          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, u, t);
+          eo_contract<P, Q, 1>(eBF, u, t);
           st_line<Q>(S0 + T::off(pb, pa, 0), t);
         }
         __syncthreads();
@@ -317,7 +381,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
           double ln[P], t[Q];
 #pragma unroll
           for (int b = 0; b < P; ++b) ln[b] = S0[T::off(qb, b, qa)];
-          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, ln, t);
+          eo_contract<P, Q, 1>(eBF, ln, t);
 #pragma unroll
           for (int o = 0; o < Q; ++o) S1[T::off(qb, o, qa)] = t[o];
         }
@@ -327,7 +391,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
           double ln[P];
 #pragma unroll
           for (int k = 0; k < P; ++k) ln[k] = aslot ? S1[T::off(k, qb, qa)] : 0.0;
-          lc<T::DOT, P, Q>(sBT, T::RQ, sB, T::RP, ln, uq);
+          eo_contract<P, Q, 1>(eBF, ln, uq);
         }
       } else {
 #pragma unroll
@@ -349,11 +413,11 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
 #pragma unroll
           for (int k = 0; k < Q; ++k) S2[T::off(k, qb, qa)] = uq[k];
         }
-        if constexpr (T::EARLY) lc<T::DOT, Q, Q>(sDT, T::RQ, sD, T::RQ, uq, g2);
+        if constexpr (T::EARLY) eo_contract<Q, Q, -1>(eDF, uq, g2);
         __syncthreads();
         // ---- 4: x and y derivatives, thread (a, b) = (qa, qb) ----
         if (aslot) {
-          line_pair<T>(sD, S2, S2, S0, S1, qa, qb);
+          line_pair<T>(eDF, S2, S2, S0, S1, qa, qb);
         }
         __syncthreads();
         // ---- 5: z-derivative of the column (still in S2) + QFunction
@@ -403,7 +467,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         __syncthreads();
         // ---- 6: x^T and y^T derivatives in place ----
         if (aslot) {
-          line_pair<T>(sDT, S0, S1, S0, S1, qa, qb);
+          line_pair<T>(eDT, S0, S1, S0, S1, qa, qb);
         }
         __syncthreads();
         // ---- 7a: column sum with the z^T derivative ----
@@ -416,7 +480,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             else
               ln[k] = aslot ? S2[T::off(k, qb, qa)] : 0.0;
           }
-          lc<T::DOT, Q, Q>(sD, T::RQ, sDT, T::RQ, ln, t);
+          eo_contract<Q, Q, -1>(eDT, ln, t);
 #pragma unroll
           for (int o = 0; o < Q; ++o) {
             const int sp = T::off(o, qb, qa);
@@ -439,7 +503,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         // ---- 7b: z^T interp of the column -> S2 [c][qj][qi] ----
         if (aslot) {
           double t[P];
-          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, w, t);
+          eo_contract<Q, P, 1>(eBT, w, t);
 #pragma unroll
           for (int k = 0; k < P; ++k) S2[T::off(k, qb, qa)] = t[k];
         }
@@ -449,7 +513,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
           double ln[Q], t[P];
 #pragma unroll
           for (int o = 0; o < Q; ++o) ln[o] = S2[T::off(qb, o, qa)];
-          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, ln, t);
+          eo_contract<Q, P, 1>(eBT, ln, t);
 #pragma unroll
           for (int j = 0; j < P; ++j) S1[T::off(qb, j, qa)] = t[j];
         }
@@ -458,7 +522,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         if (gcur.active) {
           double ln[Q], t[P];
           ld_line<Q>(S1 + T::off(pb, pa, 0), ln);
-          lc<T::DOT, Q, P>(sB, T::RP, sBT, T::RQ, ln, t);
+          eo_contract<Q, P, 1>(eBT, ln, t);
 #pragma unroll
           for (int i = 0; i < P; ++i)
             // constrained rows (y = x) are preset by the caller
