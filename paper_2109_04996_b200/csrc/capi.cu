@@ -103,7 +103,14 @@ int op_kernel_choice() {
   return choice;
 }
 
-bool pencil_disabled() { return op_kernel_choice() == 2; }
+bool pencil_disabled() {
+  // HXF_PENCIL=0: collocated sizes without a tensor-core path on the line kernel (A/B)
+  static const bool off = [] {
+    const char* v = std::getenv("HXF_PENCIL");
+    return v && v[0] == '0';
+  }();
+  return op_kernel_choice() == 2 || off;
+}
 
 bool dmma_pad_disabled() {
   static const bool off = [] {

@@ -198,8 +198,10 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
       return run_dmma_gm<3, P>(prm, s, g);
   }
   if constexpr (!INTERP) {
-    if (qk == 1 && NC == 1 && use_pencil<P, 1>() && !pencil_disabled())
-      return run_pencil_gm<P, 1>(prm, D, s, g);
+    // three components: the pencil kernel (measured ahead of the line kernel
+    // for BP6 p = 5, 8); one component: the line kernel wins at every p != 7
+    // (BP5 1e7 DOFs, K1 roof line / pencil: p=1 0.55/0.48, p=3 0.76/0.54,
+    // p=6 0.54/0.49, p=8 0.57/0.46, p=9 0.51/0.46, p=2,4,5 within 3 %)
     if (qk == 1 && NC == 3 && use_pencil<P, 3>() && !pencil_disabled())
       return run_pencil_gm<P, 3>(prm, D, s, g);
   }
