@@ -29,6 +29,7 @@
 #pragma once
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
+#include "op_eo.cuh"
 #include "op_kernel.cuh"
 #include "pcg_device.cuh"
 
@@ -63,12 +64,11 @@ struct LineTraits {
   // even-odd tables (centro-symmetric bases: M[NO-1-o][NI-1-a] = +-M[o][a]):
   // row o < ceil(NO/2) = [ (M[o][a] + M[o][a'])/2 (a < NI/2) | M[o][NI/2] (odd NI)
   // | (M[o][a] - M[o][a'])/2 ], a' = NI-1-a, for B, B^T, D, D^T
-  __host__ __device__ static constexpr int eo_rt(int ni) { return round_up(2 * (ni / 2) + 1, 2); }
   static constexpr int OFF_EBF = round_up(OFF_D + Q * RQ, 2);           // B   (Q x P)
-  static constexpr int OFF_EBT = OFF_EBF + ((Q + 1) / 2) * eo_rt(P);    // B^T (P x Q)
-  static constexpr int OFF_EDF = OFF_EBT + ((P + 1) / 2) * eo_rt(Q);    // D   (Q x Q)
-  static constexpr int OFF_EDT = OFF_EDF + ((Q + 1) / 2) * eo_rt(Q);    // D^T (Q x Q)
-  static constexpr int OFF_S = round_up(OFF_EDT + ((Q + 1) / 2) * eo_rt(Q), 2);
+  static constexpr int OFF_EBT = OFF_EBF + ((Q + 1) / 2) * eo_row_stride(P);    // B^T (P x Q)
+  static constexpr int OFF_EDF = OFF_EBT + ((P + 1) / 2) * eo_row_stride(Q);    // D   (Q x Q)
+  static constexpr int OFF_EDT = OFF_EDF + ((Q + 1) / 2) * eo_row_stride(Q);    // D^T (Q x Q)
+  static constexpr int OFF_S = round_up(OFF_EDT + ((Q + 1) / 2) * eo_row_stride(Q), 2);
   static constexpr int SMEM_BYTES = (OFF_S + EPB * 3 * SLAB) * 8;
   __device__ static __forceinline__ int off(int k, int j, int i) { return (k * Q + j) * RS + i; }
 };
@@ -83,18 +83,6 @@ struct LineGeo {
   uint32_t cmask;
   bool active;
 };
-
-// N consecutive doubles of a 16-byte aligned shared-memory row into registers
-template <int N>
-__device__ __forceinline__ void line_row(const double* src, double* d) {
-#pragma unroll
-  for (int a = 0; a + 1 < N; a += 2) {
-    const double2 v = *reinterpret_cast<const double2*>(src + a);
-    d[a] = v.x;
-    d[a + 1] = v.y;
-  }
-  if (N & 1) d[N - 1] = src[N - 1];
-}
 
 // out[o] = sum_a M[o][a] in[a] (o < NO, a < NI) in "axpy" order: column a of
 // M is the contiguous shared-memory row mt + a*str (broadcast LDS.128), so the
@@ -137,35 +125,6 @@ __device__ __forceinline__ void lc(const double* colm, int cstr, const double* r
     line_contract_dot<NI, NO>(rowm, rstr, in, out);
   else
     line_contract<NI, NO>(colm, cstr, in, out);
-}
-
-// Even-odd ("centro-symmetric") contraction: out[o] = sum_a M[o][a] in[a] for a
-// NO x NI matrix with M[NO-1-o][NI-1-a] = S M[o][a] (S = +1 interpolation,
-// -1 derivative on symmetric GLL / Gauss points), from the half-size table of
-// LineTraits (one row per output pair): half the multiply-adds and row loads.
-template <int NI, int NO, int S>
-__device__ __forceinline__ void eo_contract(const double* tab, const double* in, double* out) {
-  constexpr int HI = NI / 2, HO = (NO + 1) / 2, L = 2 * HI + 1, RT = (L + 1) / 2 * 2;
-  double e[HI > 0 ? HI : 1], f[HI > 0 ? HI : 1];
-#pragma unroll
-  for (int a = 0; a < HI; ++a) {
-    e[a] = in[a] + in[NI - 1 - a];
-    f[a] = in[a] - in[NI - 1 - a];
-  }
-#pragma unroll
-  for (int o = 0; o < HO; ++o) {
-    double row[L];
-    line_row<L>(tab + o * RT, row);
-    double E = 0.0, F = 0.0;
-#pragma unroll
-    for (int a = 0; a < HI; ++a) {
-      E += row[a] * e[a];
-      F += row[HI + 1 + a] * f[a];
-    }
-    if constexpr (NI & 1) E += row[HI] * in[HI];
-    out[o] = E + F;
-    if (NO - 1 - o != o) out[NO - 1 - o] = S > 0 ? E - F : F - E;
-  }
 }
 
 // a contiguous slab line (x-line) to / from registers
@@ -248,24 +207,13 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   const double* eDF = smem + T::OFF_EDF;
   const double* eDT = smem + T::OFF_EDT;
   for (int t = tid; t < Q * Q; t += NT) smem[T::OFF_D + (t / Q) * T::RQ + t % Q] = mats.D[t];
-  // even-odd tables from the full matrices (M(o, a) accessors)
-  auto eo_table = [&](int off, int NO, int NI, auto M) {
-    const int HI = NI / 2, RT = T::eo_rt(NI), HO = (NO + 1) / 2;
-    for (int t = tid; t < HO * RT; t += NT) {
-      const int o = t / RT, c = t % RT;
-      double v = 0.0;
-      if (c < HI) v = 0.5 * (M(o, c) + M(o, NI - 1 - c));
-      else if (c == HI) v = (NI & 1) ? M(o, HI) : 0.0;
-      else if (c < 2 * HI + 1) v = 0.5 * (M(o, c - HI - 1) - M(o, NI - 1 - (c - HI - 1)));
-      smem[off + t] = v;
-    }
-  };
+  // even-odd tables from the full matrices (op_eo.cuh)
   if constexpr (T::INTERP) {
-    eo_table(T::OFF_EBF, Q, P, [&](int o, int a) { return mats.B[o * P + a]; });
-    eo_table(T::OFF_EBT, P, Q, [&](int o, int a) { return mats.B[a * P + o]; });
+    eo_build(smem + T::OFF_EBF, Q, P, [&](int o, int a) { return mats.B[o * P + a]; }, tid, NT);
+    eo_build(smem + T::OFF_EBT, P, Q, [&](int o, int a) { return mats.B[a * P + o]; }, tid, NT);
   }
-  eo_table(T::OFF_EDF, Q, Q, [&](int o, int a) { return mats.D[o * Q + a]; });
-  eo_table(T::OFF_EDT, Q, Q, [&](int o, int a) { return mats.D[a * Q + o]; });
+  eo_build(smem + T::OFF_EDF, Q, Q, [&](int o, int a) { return mats.D[o * Q + a]; }, tid, NT);
+  eo_build(smem + T::OFF_EDT, Q, Q, [&](int o, int a) { return mats.D[a * Q + o]; }, tid, NT);
   __syncthreads();
   double* S1 = S0 + T::SLAB;
   double* S2 = S1 + T::SLAB;

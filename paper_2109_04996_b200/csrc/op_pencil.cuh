@@ -24,6 +24,7 @@
 #pragma once
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
+#include "op_eo.cuh"
 #include "pcg_device.cuh"
 
 namespace hxf {
@@ -52,9 +53,9 @@ struct PencilTraits {
   static constexpr int DR = pencil_round_up(P, 2);  // matrix row stride (16-byte rows)
   // D^T rows in shared memory too, except for p = 7 where the 512 B are what
   // it takes to fit 6 CTAs per SM (transposed rows read as D columns there)
-  static constexpr bool DT_SMEM = !SWZ;
-  static constexpr int OFF_D = 0;                   // [P][DR] D, then [P][DR] D^T
-  static constexpr int OFF_QD = (DT_SMEM ? 2 : 1) * P * DR;
+  // even-odd tables of D and D^T (op_eo.cuh; the bases are centro-symmetric)
+  static constexpr int OFF_D = 0, OFF_DT = eo_table_size(P, P);
+  static constexpr int OFF_QD = pencil_round_up(2 * eo_table_size(P, P), 2);
   static constexpr int OFF_A = OFF_QD + EPB * QDS;
   static constexpr int OFF_B = OFF_A + EPB * SLAB;
   static constexpr int OFF_C = OFF_B + EPB * SLAB;
@@ -101,7 +102,6 @@ __device__ __forceinline__ void load_row(const double* src, double* dst) {
 template <class T>
 __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   constexpr int P = T::P, PP = T::PP, P3 = T::P3, EPB = T::EPB, NT = T::NT, NC = T::NC;
-  constexpr int DR = T::DR;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_scratch[NT / 32 + 1];
@@ -112,28 +112,16 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   const int l = tid - slot * PP;
   const bool active_slot = slot < EPB;
   const int la = l % P, lb = l / P;  // (i,j) | (j,k) | (i,k) depending on the phase
-  const double* sD = smem + T::OFF_D;
-  const double* sDT = smem + T::OFF_D + P * DR;
-  // row o of D^T (= column o of D)
-  auto load_trow = [&](int o, double* d) {
-    if constexpr (T::DT_SMEM) {
-      load_row<P>(sDT + o * DR, d);
-    } else {
-#pragma unroll
-      for (int a = 0; a < P; ++a) d[a] = sD[a * DR + o];
-    }
-  };
+  const double* eD = smem + T::OFF_D;    // even-odd D
+  const double* eDT = smem + T::OFF_DT;  // even-odd D^T
   double* sQD = smem + T::OFF_QD;
   double* SA = smem + T::OFF_A + (active_slot ? slot : 0) * T::SLAB;
   double* SB = smem + T::OFF_B + (active_slot ? slot : 0) * T::SLAB;
   double* SC = smem + T::OFF_C + (active_slot ? slot : 0) * T::SLAB;
   const double* qd_el = sQD + (active_slot ? slot : 0) * T::QDS;
 
-  for (int t = tid; t < P * P; t += NT) {
-    const int r = t / P, c = t % P;
-    smem[T::OFF_D + r * DR + c] = prm.D[t];                            // D[r][c]
-    if (T::DT_SMEM) smem[T::OFF_D + P * DR + c * DR + r] = prm.D[t];  // D^T[c][r]
-  }
+  eo_build(smem + T::OFF_D, P, P, [&](int o, int a) { return prm.D[o * P + a]; }, tid, NT);
+  eo_build(smem + T::OFF_DT, P, P, [&](int o, int a) { return prm.D[a * P + o]; }, tid, NT);
 
   const int64_t nsteps = (prm.E + EPB - 1) / EPB;
   const int64_t G = gridDim.x;
@@ -236,20 +224,10 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
         if (P & 1) row[P - 1] = SA[T::off(lb, la, P - 1)];
 #pragma unroll
         for (int b = 0; b < P; ++b) col[b] = SA[T::off(lb, b, la)];
-        double gx[P];
+        double gx[P], gy[P];
+        eo_pair<P, -1>(eD, row, col, gx, gy);
 #pragma unroll
-        for (int o = 0; o < P; ++o) {
-          double d[P];
-          load_row<P>(sD + o * DR, d);
-          double sx = 0.0, sy = 0.0;
-#pragma unroll
-          for (int a = 0; a < P; ++a) {
-            sx += d[a] * row[a];
-            sy += d[a] * col[a];
-          }
-          gx[o] = sx;
-          SB[T::off(lb, o, la)] = sy;
-        }
+        for (int o = 0; o < P; ++o) SB[T::off(lb, o, la)] = gy[o];
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2)
           *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(gx[a], gx[a + 1]);
@@ -267,13 +245,11 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       load_line(gpf, (q + 2) % NC, xn);  // item q+2 lands while items q, q+1 compute
       double v2[P];
       double energy = 0.0;
+      double g2v[P];
+      eo_contract<P, P, -1>(eD, u, g2v);
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        double d[P];
-        load_row<P>(sD + k * DR, d);
-        double g2 = 0.0;
-#pragma unroll
-        for (int cc = 0; cc < P; ++cc) g2 += d[cc] * u[cc];
+        const double g2 = g2v[k];
         const int sp = T::off(k, lb, la);
         const int pt = k * PP + lb * P + la;
         const double g0 = SC[sp], g1 = SB[sp];
@@ -317,20 +293,10 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
         if (P & 1) row[P - 1] = SC[T::off(lb, la, P - 1)];
 #pragma unroll
         for (int b = 0; b < P; ++b) col[b] = SB[T::off(lb, b, la)];
-        double tx[P];
+        double tx[P], ty[P];
+        eo_pair<P, -1>(eDT, row, col, tx, ty);
 #pragma unroll
-        for (int o = 0; o < P; ++o) {
-          double d[P];
-          load_trow(o, d);
-          double sx = 0.0, sy = 0.0;
-#pragma unroll
-          for (int a = 0; a < P; ++a) {
-            sx += d[a] * row[a];
-            sy += d[a] * col[a];
-          }
-          tx[o] = sx;
-          SB[T::off(lb, o, la)] = sy;
-        }
+        for (int o = 0; o < P; ++o) SB[T::off(lb, o, la)] = ty[o];
 #pragma unroll
         for (int a = 0; a + 1 < P; a += 2)
           *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(tx[a], tx[a + 1]);
@@ -340,13 +306,11 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
 
       // ---- Z: D^T along z from registers + combine, G^T scatter ----
       if (gcur.active) {
+        double zt[P];
+        eo_contract<P, P, -1>(eDT, v2, zt);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          double d[P];
-          load_trow(k, d);
-          double s = 0.0;
-#pragma unroll
-          for (int cc = 0; cc < P; ++cc) s += d[cc] * v2[cc];
+          const double s = zt[k];
           const int sp = T::off(k, lb, la);
           const double yk = prm.coef * (SC[sp] + SB[sp] + s);
           const int64_t node = node_of(gcur, k);
