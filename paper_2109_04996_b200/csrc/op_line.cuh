@@ -27,6 +27,9 @@
 // Reference semantics: proj/src/operator.cpp:64-144, contraction.cpp:248-332,
 // qfunction.cpp:124-162.
 #pragma once
+#ifndef HXF_LINE_REGS
+#define HXF_LINE_REGS 128
+#endif
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
 #include "op_eo.cuh"
@@ -49,7 +52,10 @@ struct LineTraits {
   static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
   static constexpr int EPB = QQ >= 64 ? 1 : (128 / QQ);
   static constexpr int NT = round_up(EPB * QQ, 32);
-  static constexpr int MINB = (65536 / (NT * 128)) < 1 ? 1 : (65536 / (NT * 128) > 8 ? 8 : 65536 / (NT * 128));
+  // register target per thread (measured: 112 / 96 targets lose up to 27 % at
+  // q = 9 and 10 to spills; 128 gives 5 CTAs of 3 warps at q = 9)
+  static constexpr int REGT = HXF_LINE_REGS;
+  static constexpr int MINB = (65536 / (NT * REGT)) < 1 ? 1 : (65536 / (NT * REGT) > 8 ? 8 : 65536 / (NT * REGT));
   // odd row stride: x-line (stride RS across lanes) and column / y-line
   // (consecutive across lanes) accesses are all conflict-free (measured: a
   // 16-byte aligned RS = 2 mod 4 with LDS.128 x-lines is 20 % slower at q = 9)
