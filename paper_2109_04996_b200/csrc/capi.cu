@@ -622,6 +622,8 @@ int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* d, hxf_op** out) 
     const int n1 = d->p + 1, q = d->q;
     const int64_t S = int64_t(n1) * n1 * n1;
     if (op->P > 16) fail(HXF_EUNSUPPORTED, "hxf: p > 15 has no compiled kernel");
+    // element indices run through 32-bit fast division in the operator kernels
+    if (op->E >= (int64_t(1) << 31)) fail(HXF_EUNSUPPORTED, "hxf: 2^31 or more elements");
     if (d->indices)
       for (int64_t i = 0; i < op->E * S; ++i)
         if (d->indices[i] < 0 || d->indices[i] >= d->n_L)
