@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
     if constexpr (T::GM == 0) return g.key + k * NXY;
     return prm.idx ? (int64_t)prm.idx[g.key * P3 + la + P * (lb + P * k)] : g.key + k * NXY;
   };
+  const FastDiv divx((uint32_t)prm.nx), divy((uint32_t)prm.ny);
   auto geometry = [&](int64_t step) {
     PencilGeo g{};
     const int64_t e = step * EPB + slot;
@@ -162,13 +163,21 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
     if (T::GM == 1 && prm.idx) {
       g.key = e;
     } else {
-      const int64_t ex = e % prm.nx, r = e / prm.nx, ey = r % prm.ny, ez = r / prm.ny;
-      const int64_t ix = ex * (P - 1) + la, iy = ey * (P - 1) + lb, iz = ez * (P - 1);
+      // element lattice position (E < 2^31: 32-bit fast division)
+      const uint32_t e32 = (uint32_t)e, r = divx.div(e32), ez = divy.div(r);
+      const uint32_t ex = e32 - r * (uint32_t)prm.nx, ey = r - ez * (uint32_t)prm.ny;
+      const int64_t ix = (int64_t)ex * (P - 1) + la, iy = (int64_t)ey * (P - 1) + lb,
+                    iz = (int64_t)ez * (P - 1);
       g.key = ix + prm.NX * iy + NXY * iz;
       if (T::GM == 0 && prm.cons_mode == 1) {
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-          if (on_bnd_face(prm, ix, iy, iz + k)) g.cmask |= 1u << k;
+        // on_bnd_face along the z-line: x / y faces take the whole line
+        const int f = prm.bnd_faces;
+        const bool side = ((f & 1) && ix == 0) || ((f & 2) && ix == prm.NX - 1) ||
+                          ((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1);
+        uint32_t cm = side ? (1u << P) - 1u : 0u;
+        if ((f & 16) && iz == 0) cm |= 1u;
+        if ((f & 32) && iz + P - 1 == prm.NZ - 1) cm |= 1u << (P - 1);
+        g.cmask = cm;
       }
     }
     if (T::GM == 1 && prm.cons_mode == 2) {
