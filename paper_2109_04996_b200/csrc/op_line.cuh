@@ -50,7 +50,12 @@ struct LineTraits {
   static constexpr bool INTERP = INTERP_;
   static constexpr bool DIFF = QK == 1;  // one qdata kind per launch (1 diffusion, 2 mass)
   static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
-  static constexpr int EPB = QQ >= 64 ? 1 : (128 / QQ);
+  // elements per CTA at q = 9 as a build knob (measured: 2 loses 4-10 % on BP1/3/5,
+  // wins 8 % on BP4 only)
+#ifndef HXF_LINE_EPB81
+#define HXF_LINE_EPB81 1
+#endif
+  static constexpr int EPB = QQ == 81 ? HXF_LINE_EPB81 : (QQ >= 64 ? 1 : (128 / QQ));
   static constexpr int NT = round_up(EPB * QQ, 32);
   // register target per thread (measured: 112 / 96 targets lose up to 27 % at
   // q = 9 and 10 to spills; 128 gives 5 CTAs of 3 warps at q = 9)
