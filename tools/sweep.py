@@ -4,7 +4,9 @@ roofline fraction of each (algorithmic bytes / time / measured HBM peak).
 
 Usage: python tools/sweep.py [--bp bp5] [--p 1-15] [--sizes 1e5,1e6,1e7]
        [--deform sine] [--out profiles/r1_sweep_bp5.md]
-       [--records sweep.jsonl] [--csv sweep.csv]
+       [--records sweep.jsonl] [--csv sweep.csv] [--cpu [--cpu-iters 3]]
+--cpu times the reference itself (oracle/_ref run_bench, min of 3 reps, all
+host cores, --cpu-iters fixed CG iterations) at every point.
 --records writes one reference BenchRecord JSON per point (bench.cpp:351-363,
 P = 1 GPU) and --csv the reference's sweep CSV (bench.cpp:365-381, eta = 1 at
 P = 1; multi-GPU rows come from bench.py --gpus N and
@@ -71,6 +73,9 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--records", default=None)
     ap.add_argument("--csv", default=None)
+    ap.add_argument("--cpu", action="store_true",
+                    help="time the reference (oracle/_ref run_bench, all host cores) at each point")
+    ap.add_argument("--cpu-iters", type=int, default=3)
     a = ap.parse_args()
     peak = json.load(open(ROOT / "MEASURED_PEAKS.json"))["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
     rows = []
@@ -115,6 +120,15 @@ def main():
                        k1_us=k1 * 1e6, k1_frac=bapply / k1 / 1e9 / peak,
                        cg_us=t_it * 1e6, cg_gdofs=n / t_it / 1e9,
                        cg_frac=bcg / t_it / 1e9 / peak, setup_s=tsetup)
+            if a.cpu:
+                import os
+
+                import oracle
+                cores = os.cpu_count() or 1
+                t0 = time.perf_counter()
+                ref = oracle.run_bench_reference(a.bp, p, (d, d, d), cores, a.cpu_iters, a.deform)
+                row.update(cpu_gdofs=ref["dofs_rate"] / 1e9, cpu_cores=cores,
+                           cpu_wall_s=time.perf_counter() - t0)
             q = p + 2 if int(a.bp[2]) <= 4 else p + 1
             row["record"] = dict(bp=a.bp, p=p, q=q, E=d ** 3, n=n, P=1, iterations=a.iters,
                                  seconds=best, dofs_rate=n * a.iters / best, n_per_rank=float(n))
@@ -136,13 +150,18 @@ def main():
         with open(a.out, "w") as f:
             f.write(f"# {a.bp} throughput sweep ({a.deform} box, {a.iters} fixed CG iterations, "
                     f"HBM peak {peak} GB/s measured)\n\n")
+            cpu = a.cpu and rows
             f.write("| p | d | n (DOFs) | apply us | apply GDOF/s | apply roof | K1 us | K1 roof "
-                    "| CG us/iter | CG GDOF/s | CG roof |\n|---|---|---|---|---|---|---|---|---|---|---|\n")
+                    "| CG us/iter | CG GDOF/s | CG roof |" +
+                    (f" ref CPU GDOF/s ({rows[0]['cpu_cores']} thr) | CG speed-up |" if cpu else "") +
+                    "\n|---|---|---|---|---|---|---|---|---|---|---|" + ("---|---|" if cpu else "") + "\n")
             for r in rows:
                 f.write(f"| {r['p']} | {r['d']} | {r['n']:,} | {r['apply_us']:.1f} | "
                         f"{r['apply_gdofs']:.2f} | {r['apply_frac']:.2f} | {r['k1_us']:.1f} | "
                         f"{r['k1_frac']:.2f} | {r['cg_us']:.1f} | {r['cg_gdofs']:.2f} | "
-                        f"{r['cg_frac']:.2f} |\n")
+                        f"{r['cg_frac']:.2f} |" +
+                        (f" {r['cpu_gdofs']:.4f} | {r['cg_gdofs'] / r['cpu_gdofs']:.0f}x |" if cpu else "") +
+                        "\n")
 
 
 if __name__ == "__main__":
