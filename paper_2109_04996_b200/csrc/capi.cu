@@ -144,6 +144,14 @@ bool serpentine() {
   return on;
 }
 
+int dmma_stages() {
+  static const int ns = [] {
+    const char* v = std::getenv("HXF_DMMA_STAGES");
+    return (v && v[0] == '2') ? 2 : 1;
+  }();
+  return ns;
+}
+
 int dmma_warps() {
   static const int nw = [] {
     const char* v = std::getenv("HXF_DMMA_NW");

@@ -104,6 +104,7 @@ bool pencil_disabled();
 bool dmma_pad_disabled();     // HXF_DMMA_PAD=0: p = 4..6 back on the pencil kernel (A/B)
 bool pdl_enabled();           // HXF_PDL=1: programmatic dependent launch (off by default)
 bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward
+int dmma_stages();  // HXF_DMMA_STAGES: staged qdata buffers per CTA of op_dmma_kernel (1 default, 2)
 int dmma_warps();  // HXF_DMMA_NW: warps per element of op_dmma_kernel (2, 4 default, 8)
 int ablate_bits();
 void count_launch(int n = 1);

@@ -34,8 +34,11 @@
 
 namespace hxf {
 
-template <int NC_, int GM_, int NW_ = 4, int NP_ = 8>
+template <int NC_, int GM_, int NW_ = 4, int NP_ = 8, int NS_ = 1>
 struct DmmaTraits {
+  // NS stages of staged geometric factors (1: refill right after the
+  // QFunction consumed them; 2: two elements in flight per CTA)
+  static constexpr int NS = NS_;
   // NW warps per element; warp w owns planes / rows KK w .. KK w + KK-1
   static constexpr int P = 8, NC = NC_, GM = GM_, P3 = 512, NW = NW_, NT = 32 * NW_, KK = 8 / NW_;
   // NP = p+1 nodes per direction: 8, or 5..7 zero-padded to the 8^3 tile
@@ -51,7 +54,7 @@ struct DmmaTraits {
   static constexpr int SLAB = 512;   // doubles
   static constexpr int QDS = 6 * NP3;
   static constexpr int OFF_QD = 0;
-  static constexpr int OFF_A = QDS;  // U, then V0
+  static constexpr int OFF_A = NS_ * QDS;  // U, then V0
   static constexpr int OFF_B = OFF_A + SLAB;  // V1, then Y2 (dist-Z -> dist-X transpose)
   static constexpr int OFF_Z = OFF_B + SLAB;  // G2, then V2
   static constexpr int SMEM_BYTES = (OFF_Z + SLAB) * 8;
@@ -72,7 +75,7 @@ template <class T>
 __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams prm) {
   constexpr int NC = T::NC, P3 = T::P3, NT = T::NT, KK = T::KK;
   extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t qbar;
+  __shared__ __align__(8) uint64_t qbars[T::NS];
   __shared__ double red_scratch[NT / 32 + 1];
 
   const int tid = threadIdx.x;
@@ -103,23 +106,31 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     const int64_t k = prm.rev ? nsteps - 1 - s : s;
     return prm.elist ? (int64_t)__ldg(prm.elist + k) : k;  // subset (partition overlap)
   };
-  auto issue_qdata = [&](int64_t e) {
-    mbar_arrive_expect_tx(&qbar, (uint32_t)(T::QDS * 8));
-    bulk_g2s(sQD, prm.qd + elem(e) * T::QDS, (uint32_t)(T::QDS * 8), &qbar, policy);
+  // sweep step s of this CTA goes to stage (s / G) % NS
+  auto issue_qdata = [&](int64_t e, int stage) {
+    mbar_arrive_expect_tx(&qbars[stage], (uint32_t)(T::QDS * 8));
+    bulk_g2s(sQD + stage * T::QDS, prm.qd + elem(e) * T::QDS, (uint32_t)(T::QDS * 8), &qbars[stage],
+             policy);
   };
   // the first element's factors do not depend on the previous kernel: request
   // them before the PDL wait so the copy overlaps that kernel's tail
   const bool first_qd = (int64_t)blockIdx.x < nsteps && !(prm.ablate & 4);
   if (tid == 0) {
-    mbar_init(&qbar, 1);
+    for (int i = 0; i < T::NS; ++i) mbar_init(&qbars[i], 1);
     fence_mbar_init();
     policy = l2_evict_first_policy();
-    if (first_qd) issue_qdata(blockIdx.x);
+    if (first_qd) {
+      issue_qdata(blockIdx.x, 0);
+      if (T::NS > 1 && (int64_t)blockIdx.x + G < nsteps) issue_qdata(blockIdx.x + G, 1);
+    }
   }
   pdl_wait();     // x, y, stop and the PCG state come from the previous kernels
   // (no early trigger: dependents launch when this grid completes)
   if (prm.stop && *prm.stop) {
-    if (tid == 0 && first_qd) mbar_wait(&qbar, 0);  // no copy in flight at exit
+    if (tid == 0 && first_qd) {  // no copy in flight at exit
+      mbar_wait(&qbars[0], 0);
+      if (T::NS > 1 && (int64_t)blockIdx.x + G < nsteps) mbar_wait(&qbars[1], 0);
+    }
     return;
   }
 
@@ -303,7 +314,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dr[ks], SA[T::off(4 * ks + t, j, g)]);
         *reinterpret_cast<double2*>(SZ + T::off(g, j, 2 * t)) = make_double2(c0, c1);  // dist Z
       }
-      if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
+      const int stg = T::NS > 1 ? (it & 1) : 0;
+      const double* sQDs = sQD + stg * T::QDS;
+      if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbars[stg], (uint32_t)((it / T::NS) & 1));
       __syncthreads();  // (B) G2 complete, slab A free
 
       // ---- QFunction on dist X (qfunction.cpp:135-162) ----
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         if constexpr (!T::PAD) {
           const int pt = k * 64 + g * 8 + 2 * t;
 #pragma unroll
-          for (int m = 0; m < 6; ++m) s[m] = *reinterpret_cast<const double2*>(sQD + m * P3 + pt);
+          for (int m = 0; m < 6; ++m) s[m] = *reinterpret_cast<const double2*>(sQDs + m * P3 + pt);
         } else {
           // compact NP^3 factors; padding points get 0 (their V is then 0)
           constexpr int NP = T::NP;
@@ -325,8 +338,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
           const bool v0 = k < NP && g < NP && 2 * t < NP, v1 = k < NP && g < NP && 2 * t + 1 < NP;
 #pragma unroll
           for (int m = 0; m < 6; ++m) {
-            s[m].x = v0 ? sQD[m * T::NP3 + pt] : 0.0;
-            s[m].y = v1 ? sQD[m * T::NP3 + pt + 1] : 0.0;
+            s[m].x = v0 ? sQDs[m * T::NP3 + pt] : 0.0;
+            s[m].y = v1 ? sQDs[m * T::NP3 + pt + 1] : 0.0;
           }
         }
         double v0[2], v1[2], v2[2];
@@ -350,7 +363,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       dot_acc += prm.coef * energy;
       if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
       __syncthreads();  // (C) V0, V1, V2 complete
-      if (c == NC - 1 && tid == 0 && e + G < nsteps && !(prm.ablate & 4)) issue_qdata(e + G);
+      if (c == NC - 1 && tid == 0 && e + T::NS * G < nsteps && !(prm.ablate & 4))
+        issue_qdata(e + T::NS * G, stg);
 
       // ---- transposed contractions ----
       double y01[KK][2];

@@ -149,6 +149,12 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
 
 template <int NC, int NW, int NP = 8>
 cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
+  if constexpr (NP == 8 && NW == 4) {
+    if (dmma_stages() == 2) {
+      if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW, NP, 2>>(prm, s, g);
+      return run_dmma<DmmaTraits<NC, 1, NW, NP, 2>>(prm, s, g);
+    }
+  }
   if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW, NP>>(prm, s, g);
   return run_dmma<DmmaTraits<NC, 1, NW, NP>>(prm, s, g);
 }
