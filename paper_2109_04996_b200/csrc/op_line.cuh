@@ -27,6 +27,11 @@
 // Reference semantics: proj/src/operator.cpp:64-144, contraction.cpp:248-332,
 // qfunction.cpp:124-162.
 #pragma once
+// z-derivative kept in registers up to q = 10 (measured: q = 12 in registers spills,
+// BP5 p=11 K1 363 -> 261 us and BP3 p=15 574 -> 505 us with the late form)
+#ifndef HXF_LINE_EARLY_Q
+#define HXF_LINE_EARLY_Q 10
+#endif
 #ifndef HXF_LINE_REGS
 #define HXF_LINE_REGS 128
 #endif
@@ -46,7 +51,7 @@ struct LineTraits {
   static constexpr bool DOT = DOT_;
   // z-derivative / v2 of the column kept in registers across phases 4-7
   // (measured faster at q = 9); larger q recompute it from S2 in phase 5
-  static constexpr bool EARLY = Q <= 12 || Q >= 16;
+  static constexpr bool EARLY = Q <= HXF_LINE_EARLY_Q;
   static constexpr bool INTERP = INTERP_;
   static constexpr bool DIFF = QK == 1;  // one qdata kind per launch (1 diffusion, 2 mass)
   static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
