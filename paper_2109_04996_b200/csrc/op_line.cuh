@@ -29,6 +29,11 @@
 #pragma once
 // z-derivative kept in registers up to q = 10 (measured: q = 12 in registers spills,
 // BP5 p=11 K1 363 -> 261 us and BP3 p=15 574 -> 505 us with the late form)
+// threads per CTA targeted for q <= 4 (several elements per CTA; measured 64 ahead
+// of 128 by 2-8 % for q = 2..4 and of 256 by 5-15 %), 128 for q = 5..7
+#ifndef HXF_LINE_SMALL_NT
+#define HXF_LINE_SMALL_NT 64
+#endif
 #ifndef HXF_LINE_EARLY_Q
 #define HXF_LINE_EARLY_Q 10
 #endif
@@ -60,7 +65,8 @@ struct LineTraits {
 #ifndef HXF_LINE_EPB81
 #define HXF_LINE_EPB81 1
 #endif
-  static constexpr int EPB = QQ == 81 ? HXF_LINE_EPB81 : (QQ >= 64 ? 1 : (128 / QQ));
+  static constexpr int EPB =
+      QQ == 81 ? HXF_LINE_EPB81 : (QQ >= 64 ? 1 : ((QQ <= 16 ? HXF_LINE_SMALL_NT : 128) / QQ));
   static constexpr int NT = round_up(EPB * QQ, 32);
   // register target per thread (measured: 112 / 96 targets lose up to 27 % at
   // q = 9 and 10 to spills; 128 gives 5 CTAs of 3 warps at q = 9)
