@@ -163,6 +163,22 @@ int dmma_warps() {
 
 int max_op_grid() { return num_sms() * 32; }
 
+bool centro_symmetric(int P, int Q, bool interp, const double* B, const double* D) {
+  auto close = [](double a, double b, double scale) { return std::fabs(a - b) <= 1e-13 * scale; };
+  double sb = 0, sd = 0;
+  for (int i = 0; i < Q * P; ++i) sb = std::fmax(sb, std::fabs(B[i]));
+  for (int i = 0; i < Q * Q; ++i) sd = std::fmax(sd, std::fabs(D[i]));
+  for (int o = 0; o < Q; ++o)
+    for (int a = 0; a < Q; ++a)
+      if (!close(D[(Q - 1 - o) * Q + (Q - 1 - a)], -D[o * Q + a], sd)) return false;
+  if (interp)
+    for (int o = 0; o < Q; ++o)
+      for (int a = 0; a < P; ++a)
+        if (!close(B[(Q - 1 - o) * P + (P - 1 - a)], B[o * P + a], sb)) return false;
+  return true;
+}
+
+
 cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams& prm,
                       const double* B, const double* D, cudaStream_t s, int* grid_out) {
   switch (P) {
@@ -242,9 +258,13 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   // partitioned, one diffusion pass on the DMMA kernel: boundary elements,
   // fork the sum-exchange of the interface planes (only boundary elements
   // touch them) onto the comm stream, interior elements meanwhile, join
+  // (kernels that take an element list: DMMA (p = 7 collocated) and the line
+  // kernel (interpolating bases, one-component collocated p != 7, p >= 10))
+  const bool dmma_path = op->P == 8 && !op->interp && op_kernel_choice() == 0;
+  const bool line_path = op_kernel_choice() != 2 && op->symmetric &&
+                         (op->interp || (op->P != 8 && (op->m == 1 || op->P > 10)));
   const bool split = halo && op->comm && op->d_elist && op->n_bnd > 0 && op->n_int > 0 &&
-                     op->beta == 0.0 && op->P == 8 && !op->interp && op_kernel_choice() == 0 &&
-                     overlap_enabled();
+                     op->beta == 0.0 && (dmma_path || line_path) && overlap_enabled();
   if (split) {
     prm.elist = op->d_elist;
     prm.E = op->n_bnd;
@@ -662,6 +682,7 @@ int hxf_operator_create(hxf_ctx* ctx, const hxf_operator_desc* d, hxf_op** out) 
     } else {
       fail(HXF_EUNSUPPORTED, "hxf: basis needs q = p+1 collocated GLL or q = p+2");
     }
+    op->symmetric = centro_symmetric(op->P, op->Q, op->interp, op->B.data(), op->Dq.data());
     // restriction: structured lattice or int32 table
     op->structured = detect_structured(op.get(), d->indices, d->dims);
     if (!op->structured) {

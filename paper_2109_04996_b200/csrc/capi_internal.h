@@ -71,6 +71,7 @@ struct hxf_op {
   int p = 0, q = 0, m = 1, P = 0, Q = 0;
   int64_t E = 0, n_L = 0;
   bool interp = false;
+  bool symmetric = false;  // centro-symmetric 1-D matrices (even-odd kernels usable)
   std::vector<double> B, Dq;  // kernel-parameter matrices
   double alpha = 0, beta = 0;
   bool structured = false;

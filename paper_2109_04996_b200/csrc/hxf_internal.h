@@ -74,6 +74,11 @@ cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams&
 // Upper bound on the grid of any launch_op() call (partials buffer size).
 int max_op_grid();
 
+// The even-odd line / pencil kernels need centro-symmetric 1-D matrices
+// (B[q-1-i][p-j] = B[i][j], D[q-1-i][q-1-j] = -D[i][j]); otherwise the general
+// kernel runs.
+bool centro_symmetric(int P, int Q, bool interp, const double* B, const double* D);
+
 // Per-P launchers (op_inst_p*.cu)
 #define HXF_DECL_P(N)                                                                          \
   cudaError_t launch_op_p##N(int Q, int NC, bool interp, int qk, const OpParams& prm,       \

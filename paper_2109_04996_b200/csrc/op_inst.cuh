@@ -34,6 +34,7 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
     if (nb < 1) return cudaErrorInvalidConfiguration;
     max_ctas = nb * num_sms();
   }
+  if (prm.elist) return cudaErrorNotSupported;  // no element-list support
   OpMats<T::P, T::Q> mats;
   std::memset(&mats, 0, sizeof mats);
   if (T::INTERP) std::memcpy(mats.B, B, sizeof(double) * T::Q * T::P);
@@ -51,21 +52,6 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
 // (B[q-1-i][p-j] = B[i][j], D[q-1-i][q-1-j] = -D[i][j]: symmetric GLL nodes and
 // Gauss / GLL points, make_basis, tensor_basis.cpp:40-71).  Anything else
 // takes the general kernel.
-inline bool centro_symmetric(int P, int Q, bool interp, const double* B, const double* D) {
-  auto close = [](double a, double b, double scale) { return std::fabs(a - b) <= 1e-13 * scale; };
-  double sb = 0, sd = 0;
-  for (int i = 0; i < Q * P; ++i) sb = std::fmax(sb, std::fabs(B[i]));
-  for (int i = 0; i < Q * Q; ++i) sd = std::fmax(sd, std::fabs(D[i]));
-  for (int o = 0; o < Q; ++o)
-    for (int a = 0; a < Q; ++a)
-      if (!close(D[(Q - 1 - o) * Q + (Q - 1 - a)], -D[o * Q + a], sd)) return false;
-  if (interp)
-    for (int o = 0; o < Q; ++o)
-      for (int a = 0; a < P; ++a)
-        if (!close(B[(Q - 1 - o) * P + (P - 1 - a)], B[o * P + a], sb)) return false;
-  return true;
-}
-
 // Line kernel (op_line.cuh): interpolating bases and the large collocated sizes.
 template <class T>
 cudaError_t run_line(const OpParams& prm, const double* B, const double* D, cudaStream_t s,
@@ -113,6 +99,7 @@ cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int
   }
   static_assert(T::GM == 0 || T::GM == 1, "gather mode");
   (void)D;
+  if (prm.elist) return cudaErrorNotSupported;  // no element-list support
   if (!prm.D) return cudaErrorInvalidValue;
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
   const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);

@@ -250,11 +250,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   const int64_t NXY = prm.NX * prm.NY;
 
   const FastDiv divx((uint32_t)prm.nx), divy((uint32_t)prm.ny);
+  // work slot -> element (a subset list for the partitioned overlap, else identity)
+  auto elem_of = [&](int64_t k) -> int64_t { return prm.elist ? (int64_t)__ldg(prm.elist + k) : k; };
   auto geometry = [&](int64_t step) {
     LineGeo g{};
-    const int64_t e = step * EPB + slot;
-    g.active = gthread && step < nsteps && e < prm.E;
+    const int64_t k = step * EPB + slot;
+    g.active = gthread && step < nsteps && k < prm.E;
     if (!g.active) return g;
+    const int64_t e = elem_of(k);
     const int li = T::INTERP ? 0 : qa, lj = T::INTERP ? pa : qb, lk = T::INTERP ? pb : 0;
     if (prm.idx) {
       g.tab = e * T::P3 + li + P * (lj + P * lk);
@@ -310,9 +313,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   // L2 prefetch of a step's geometric factors (bulk, no shared memory)
   auto prefetch_qd = [&](int64_t step) {
     if (step < nsteps) {
-      const int64_t e0 = step * EPB;
-      const int ne = (int)((prm.E - e0) < EPB ? (prm.E - e0) : EPB);
-      bulk_prefetch_l2(prm.qd + e0 * T::QDS, (uint32_t)(ne * T::QDS * 8));
+      const int64_t k0 = step * EPB;
+      const int ne = (int)((prm.E - k0) < EPB ? (prm.E - k0) : EPB);
+      if (prm.elist) {
+        for (int i = 0; i < ne; ++i)
+          bulk_prefetch_l2(prm.qd + elem_of(k0 + i) * T::QDS, (uint32_t)(T::QDS * 8));
+      } else {
+        bulk_prefetch_l2(prm.qd + k0 * T::QDS, (uint32_t)(ne * T::QDS * 8));
+      }
     }
   };
   if (tid == 0) prefetch_qd(blockIdx.x);
@@ -324,9 +332,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   double dot_acc = 0.0;
 #pragma unroll 1
   for (int64_t step = blockIdx.x; step < nsteps; step += G) {
-    const int64_t e = step * EPB + slot;
-    const bool eactive = aslot && e < prm.E;
-    const double* qd_el = prm.qd + (eactive ? e : 0) * T::QDS;
+    const int64_t ks = step * EPB + slot;
+    const bool eactive = aslot && ks < prm.E;
+    const double* qd_el = prm.qd + (eactive ? elem_of(ks) : 0) * T::QDS;
     if (tid == 0) prefetch_qd(step + G);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {

@@ -20,6 +20,8 @@ from paper_2109_04996_b200 import _core
 pytestmark = pytest.mark.gpu
 
 CASES = [
+    # line kernel (interpolating bases, one-component collocated p != 7): the
+    # boundary-first split with the exchange forked under the interior elements
     ("bp5", 4, (4, 3, 2), "sine", 2),
     ("bp5", 3, (4, 4, 2), "sine", 8),
     ("bp3", 3, (4, 3, 3), "sine", 4),
