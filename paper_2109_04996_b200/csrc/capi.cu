@@ -144,6 +144,14 @@ bool serpentine() {
   return on;
 }
 
+bool xbatch() {  // HXF_XBATCH=0: x += alpha p every iteration (A/B)
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_XBATCH");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int dmma_stages() {
   static const int ns = [] {
     const char* v = std::getenv("HXF_DMMA_STAGES");
@@ -394,6 +402,7 @@ void pcg_prepare(hxf_op* op, int limit) {
   const size_t n = size_t(op->size());
   op->w_r.ensure(n);
   op->w_p.ensure(n);
+  if (xbatch()) op->w_p2.ensure(n);
   op->w_Ap.ensure(n);
   op->w_vpart.ensure(size_t(3 * vec_grid()));  // per-CTA partials (<= 3 per CTA)
   op->w_hist.ensure(size_t(limit) + 2);
@@ -411,7 +420,13 @@ void pcg_enqueue_init(const PcgSolve& ps, cudaStream_t s) {
 
 void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capturing) {
   hxf_op* op = ps.op;
-  double *r = op->w_r.p, *p = op->w_p.p, *Ap = op->w_Ap.p, *vpart = op->w_vpart.p;
+  // batched x updates: p alternates between two buffers (iteration it reads
+  // its p from A when odd, B when even) so the previous direction survives
+  const bool xb = xbatch();
+  double *r = op->w_r.p, *Ap = op->w_Ap.p, *vpart = op->w_vpart.p;
+  double* pA = op->w_p.p;
+  double* pB = xb ? op->w_p2.p : op->w_p.p;
+  double* p = (xb && !(it & 1)) ? pB : pA;
   double* red = state_red(op);
   auto record = [&](cudaEvent_t e) {
     // (External: inside a captured graph the record is a real timing event)
@@ -435,8 +450,11 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
                        serp & odd),
      "pcg update");
   op_allreduce(op, red + 1, 2, s);  // r.r, r.z
+  const int xmode = !xb ? 0 : ((it & 1) ? 1 : 2);
+  double* pout = !xb ? pA : ((it & 1) ? pB : pA);
   ck(pcg_launch_direction(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,
-                          Ap, op->d_mask, op->d_own, vpart, serp & (odd ^ 1)),
+                          xmode == 2 ? pA : nullptr, pout, Ap, op->d_mask, op->d_own, vpart,
+                          serp & (odd ^ 1), xmode),
      "pcg direction");
 }
 

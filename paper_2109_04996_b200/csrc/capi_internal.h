@@ -89,7 +89,7 @@ struct hxf_op {
   double* d_part = nullptr;
   double *d_B = nullptr, *d_G = nullptr, *d_Bt = nullptr, *d_Gt = nullptr;
   double *d_bb = nullptr, *d_dd = nullptr, *d_bd = nullptr;
-  DevVec w_x, w_y, w_r, w_p, w_Ap, w_b, w_d, w_dinv, w_vpart, w_hist, w_ediag, w_ldiag;
+  DevVec w_x, w_y, w_r, w_p, w_p2, w_Ap, w_b, w_d, w_dinv, w_vpart, w_hist, w_ediag, w_ldiag;
   PcgState* d_state = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
@@ -140,7 +140,7 @@ struct hxf_op {
                       (void*)d_part, (void*)d_B, (void*)d_G, (void*)d_Bt, (void*)d_Gt,
                       (void*)d_bb, (void*)d_dd, (void*)d_bd, (void*)d_state, (void*)d_own, (void*)d_elist})
       if (ptr) cudaFree(ptr);
-    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
+    for (DevVec* v : {&w_x, &w_y, &w_r, &w_p, &w_p2, &w_Ap, &w_b, &w_d, &w_dinv, &w_vpart, &w_hist, &w_ediag,
                       &w_ldiag, &w_halo, &w_b2, &w_x2, &w_states, &w_hists})
       v->release();
     for (auto e : ev) cudaEventDestroy(e);

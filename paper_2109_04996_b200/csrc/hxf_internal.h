@@ -21,6 +21,7 @@ enum PcgError { PCG_OK = 0, PCG_ERR_RHS = 1, PCG_ERR_APPLY_NAN = 2, PCG_ERR_INDE
 struct PcgState {
   double red[8];
   double rho, pap, alpha, beta, norm_b, target, res, tol;
+  double alpha_prev;  // alpha of the previous iteration (x updates batched in pairs)
   int it, stop, converged, error, limit, fixed;
   unsigned int counter[4];  // last-block counters: K1, update, direction, init
 };
@@ -109,7 +110,8 @@ bool pencil_disabled();
 bool dmma_pad_disabled();     // HXF_DMMA_PAD=0: p = 4..6 back on the pencil kernel (A/B)
 bool pdl_enabled();           // HXF_PDL=1: programmatic dependent launch (off by default)
 bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward
-int dmma_stages();  // HXF_DMMA_STAGES: staged qdata buffers per CTA of op_dmma_kernel (1 default, 2)
+int dmma_stages();
+bool xbatch();  // PCG x updates batched over iteration pairs (HXF_XBATCH=0 disables)  // HXF_DMMA_STAGES: staged qdata buffers per CTA of op_dmma_kernel (1 default, 2)
 int dmma_warps();  // HXF_DMMA_NW: warps per element of op_dmma_kernel (2, 4 default, 8)
 int ablate_bits();
 void count_launch(int n = 1);

@@ -224,12 +224,27 @@ template <bool VEC>
 __global__ void __launch_bounds__(VT, 4)
     pcg_direction_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                          const double* __restrict__ d, const double* __restrict__ r,
-                         double* __restrict__ x, double* __restrict__ p, double* __restrict__ Ap,
-                         const uint32_t* cons_mask, const uint32_t* own, double* part, int rev) {
+                         double* __restrict__ x, const double* p, const double* pprev, double* pout,
+                         double* __restrict__ Ap, const uint32_t* cons_mask, const uint32_t* own,
+                         double* part, int rev, int xmode) {
   __shared__ double scratch[VT / 32];
   pdl_wait();
-  if (st->stop) return;  // stopped by the update kernel (pAp check): x untouched
+  if (st->stop) {
+    // stopped by the update kernel (pAp check, pcg.cpp:74-82): x gets only the
+    // update still pending from the previous iteration (batched mode)
+    if (xmode == 2 && !st->error) {
+      const double ap = st->alpha_prev;
+      const int64_t n = n_L * m, stride = (int64_t)gridDim.x * VT;
+      for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += stride)
+        x[i] = fma(ap, pprev[i], x[i]);
+    }
+    return;
+  }
   const double alpha = st->alpha;
+  // xmode 0: x += alpha p; 1: deferred to the next iteration (unless
+  // stopping); 2: x += alpha_prev p_prev + alpha p (same rounding sequence as
+  // two single updates: x <- fma(alpha, p, fma(alpha_prev, p_prev, x)))
+  const double alpha_prev = xmode == 2 ? st->alpha_prev : 0.0;
   const double rr = st->red[1], rz = st->red[2];
   const double res = sqrt(rr);
   const double rho = st->rho;
@@ -248,18 +263,29 @@ __global__ void __launch_bounds__(VT, 4)
       const int64_t h = n_L / 2;  // n_L even
       const double2* r2 = reinterpret_cast<const double2*>(r + o);
       const double2* d2 = reinterpret_cast<const double2*>(d + o);
-      double2* p2 = reinterpret_cast<double2*>(p + o);
+      const double2* p2 = reinterpret_cast<const double2*>(p + o);
+      const double2* pp2 = reinterpret_cast<const double2*>((xmode == 2 ? pprev : p) + o);
+      double2* po2 = reinterpret_cast<double2*>(pout + o);
       double2* a2 = reinterpret_cast<double2*>(Ap + o);
       double2* x2 = reinterpret_cast<double2*>(x + o);
-      auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv, double2 xv) {
-        xv.x += alpha * pv.x;
-        xv.y += alpha * pv.y;
-        x2[k] = xv;
+      const bool xupd = xmode != 1 || stop;
+      auto two = [&](int64_t k, double2 rv, double2 pv, double2 dv) {
+        if (xupd) {
+          double2 xv = x2[k];
+          if (xmode == 2) {
+            const double2 qv = pp2[k];
+            xv.x = fma(alpha_prev, qv.x, xv.x);
+            xv.y = fma(alpha_prev, qv.y, xv.y);
+          }
+          xv.x = fma(alpha, pv.x, xv.x);
+          xv.y = fma(alpha, pv.y, xv.y);
+          x2[k] = xv;
+        }
         if (stop) return;
         double2 q;
         q.x = rv.x * dv.x + beta * pv.x;  // dv = 1/diag (or 1)
         q.y = rv.y * dv.y + beta * pv.y;
-        p2[k] = q;
+        po2[k] = q;
         const int64_t node = 2 * k;
         uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
         if (own) w &= (own[node >> 5] >> (node & 31)) & 3u;
@@ -271,28 +297,31 @@ __global__ void __launch_bounds__(VT, 4)
       int64_t j = tid;
       for (; j + stride < h; j += 2 * stride) {
         const int64_t k = rev ? h - 1 - j : j, k1 = rev ? k - stride : k + stride;
-        const double2 pa = p2[k], xa = x2[k];
-        const double2 pb = p2[k1], xb = x2[k1];
+        const double2 pa = p2[k], pb = p2[k1];
         const double2 ra = stop ? one2 : r2[k], da = (d && !stop) ? d2[k] : one2;
         const double2 rb = stop ? one2 : r2[k1], db = (d && !stop) ? d2[k1] : one2;
-        two(k, ra, pa, da, xa);
-        two(k1, rb, pb, db, xb);
+        two(k, ra, pa, da);
+        two(k1, rb, pb, db);
       }
       if (j < h) {
         const int64_t k = rev ? h - 1 - j : j;
-        two(k, stop ? one2 : r2[k], p2[k], (d && !stop) ? d2[k] : one2, x2[k]);
+        two(k, stop ? one2 : r2[k], p2[k], (d && !stop) ? d2[k] : one2);
       }
     } else {
       for (int64_t jn = tid; jn < n_L; jn += stride) {
         const int64_t node = rev ? n_L - 1 - jn : jn;
         const int64_t i = o + node;
         const double po = p[i];
-        x[i] += alpha * po;
+        if (xmode != 1 || stop) {
+          double xv = x[i];
+          if (xmode == 2) xv = fma(alpha_prev, pprev[i], xv);
+          x[i] = fma(alpha, po, xv);
+        }
         if (stop) continue;
         const double zi = d ? r[i] * d[i] : r[i];  // d holds 1/diag here
         const double pi = zi + beta * po;
         const bool cw = is_cons(cons_mask, node) && owned_w(own, node) != 0.0;
-        p[i] = pi;
+        pout[i] = pi;
         Ap[i] = cw ? pi : 0.0;  // next RED target; constrained rows preset to A p = p
         if (cw) cc += pi * pi;
       }
@@ -323,6 +352,7 @@ __global__ void __launch_bounds__(VT, 4)
     if (conv) st->converged = 1;
     st->beta = beta;
     st->rho = rz;
+    st->alpha_prev = alpha;
   }
 }
 
@@ -382,14 +412,15 @@ cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L,
 }
 
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
-                                 int m, const double* d, const double* r, double* x, double* p,
-                                 double* Ap, const uint32_t* mask, const uint32_t* own, double* part,
-                                 int rev) {
+                                 int m, const double* d, const double* r, double* x, const double* p,
+                                 const double* pprev, double* pout, double* Ap,
+                                 const uint32_t* mask, const uint32_t* own, double* part, int rev,
+                                 int xmode) {
   const bool vec = (n_L % 2) == 0 && aligned16(d) && aligned16(r) && aligned16(x) &&
-                   aligned16(p) && aligned16(Ap);
+                   aligned16(p) && aligned16(pprev) && aligned16(pout) && aligned16(Ap);
   auto k = vec ? pcg_direction_kernel<true> : pcg_direction_kernel<false>;
   const cudaError_t err = launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, hist, n_L, m, d,
-                                     r, x, p, Ap, mask, own, part, rev);
+                                     r, x, p, pprev, pout, Ap, mask, own, part, rev, xmode);
   count_launch();
   return err;
 }

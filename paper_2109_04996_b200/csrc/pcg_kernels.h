@@ -17,9 +17,13 @@ cudaError_t pcg_launch_init_finalize(cudaStream_t s, PcgState* st, double* hist)
 cudaError_t pcg_launch_update(cudaStream_t s, PcgState* st, int it, int64_t n_L, int m,
                               const double* d, double* r, const double* Ap, const uint32_t* own,
                               double* part, int rev = 0);
+// xmode 0: x += alpha p; 1: x update deferred (p_next -> pout, p kept); 2:
+// x += alpha_prev pprev + alpha p (x updates of iteration pairs batched: one
+// vector pass less per two iterations)
 cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L,
-                                 int m, const double* d, const double* r, double* x, double* p,
-                                 double* Ap, const uint32_t* mask, const uint32_t* own,
-                                 double* part, int rev = 0);
+                                 int m, const double* d, const double* r, double* x, const double* p,
+                                 const double* pprev, double* pout, double* Ap,
+                                 const uint32_t* mask, const uint32_t* own, double* part,
+                                 int rev, int xmode);
 
 }  // namespace hxf
