@@ -30,6 +30,9 @@
 #pragma once
 // CTAs per SM the register budget targets (measured: 5 -> 96 registers, no spills,
 // but 2.5 % slower at C3 and 9 % at C4 p=7 than 4 -> 128 registers)
+#ifndef HXF_DMMA_MINB3
+#define HXF_DMMA_MINB3 4
+#endif
 #ifndef HXF_DMMA_MINB
 #define HXF_DMMA_MINB 4
 #endif
@@ -55,7 +58,7 @@ struct DmmaTraits {
   static_assert(NW_ == 2 || NW_ == 4 || NW_ == 8, "8 planes split over NW warps");
   // CTAs per SM the register budget is sized for (tuned at C3: NW = 4 -> 122
   // registers, 4 CTAs; NW = 2 needs 224 registers to keep its loads in flight)
-  static constexpr int MINB = NW_ == 8 ? 3 : HXF_DMMA_MINB;
+  static constexpr int MINB = NW_ == 8 ? 3 : (NC_ == 3 ? HXF_DMMA_MINB3 : HXF_DMMA_MINB);
   static constexpr int SLAB = 512;   // doubles
   static constexpr int QDS = 6 * NP3;
   static constexpr int OFF_QD = 0;
