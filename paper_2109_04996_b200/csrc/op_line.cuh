@@ -3,10 +3,12 @@
 // no tensor-core or pencil path (p >= 10).
 //
 // Every 1-D contraction is a register "line": one thread loads the Q (or P)
-// values of one line of the element's slab, multiplies by the 1-D matrix whose
-// entries are kernel-parameter constants (uniform, fully unrolled indices, so
-// they are constant-bank operands of DFMA — no load per multiply-add) and
-// writes the line back.  Phases (one __syncthreads between each):
+// values of one line of the element's slab and applies the 1-D matrix in
+// even-odd form (op_eo.cuh: half-size tables broadcast from shared memory as
+// LDS.128 rows, half the multiply-adds of the plain product; on sm_100 DFMA
+// cannot take an FP64 constant-bank operand, so kernel-parameter matrices
+// would cost a uniform-register move per use) and writes the line back.
+// Phases (one __syncthreads between each):
 //   1  x-interp  thread (j,k) gathers its node x-line straight from global
 //      memory (software-pipelined one element ahead) -> S0 [k][j][qi]
 //   2  y-interp  thread (qi,k)                        -> S1 [k][qj][qi]
@@ -48,12 +50,9 @@
 
 namespace hxf {
 
-template <int P_, int Q_, int NC_, int QK_, bool INTERP_, bool DOT_ = false>
+template <int P_, int Q_, int NC_, int QK_, bool INTERP_>
 struct LineTraits {
   static constexpr int P = P_, Q = Q_, NC = NC_, QK = QK_;
-  // contraction order: axpy (independent accumulators) or dot; measured
-  // equal at q = 9, 12, 14
-  static constexpr bool DOT = DOT_;
   // z-derivative / v2 of the column kept in registers across phases 4-7
   // (measured faster at q = 9); larger q recompute it from S2 in phase 5
   static constexpr bool EARLY = Q <= HXF_LINE_EARLY_Q;
@@ -105,49 +104,6 @@ struct LineGeo {
   uint32_t cmask;
   bool active;
 };
-
-// out[o] = sum_a M[o][a] in[a] (o < NO, a < NI) in "axpy" order: column a of
-// M is the contiguous shared-memory row mt + a*str (broadcast LDS.128), so the
-// NO accumulators are independent chains; each sum still runs over a in
-// increasing order (contraction.cpp:26-73).
-template <int NI, int NO>
-__device__ __forceinline__ void line_contract(const double* mt, int str, const double* in,
-                                              double* out) {
-#pragma unroll
-  for (int o = 0; o < NO; ++o) out[o] = 0.0;
-#pragma unroll
-  for (int a = 0; a < NI; ++a) {
-    double col[NO];
-    line_row<NO>(mt + a * str, col);
-#pragma unroll
-    for (int o = 0; o < NO; ++o) out[o] += col[o] * in[a];
-  }
-}
-
-// the same contraction in "dot" order: row o of M is the shared-memory row
-// m + o*str (one dependent chain per output)
-template <int NI, int NO>
-__device__ __forceinline__ void line_contract_dot(const double* m, int str, const double* in,
-                                                  double* out) {
-#pragma unroll
-  for (int o = 0; o < NO; ++o) {
-    double row[NI];
-    line_row<NI>(m + o * str, row);
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < NI; ++a) s += row[a] * in[a];
-    out[o] = s;
-  }
-}
-
-template <bool DOT, int NI, int NO>
-__device__ __forceinline__ void lc(const double* colm, int cstr, const double* rowm, int rstr,
-                                   const double* in, double* out) {
-  if constexpr (DOT)
-    line_contract_dot<NI, NO>(rowm, rstr, in, out);
-  else
-    line_contract<NI, NO>(colm, cstr, in, out);
-}
 
 // a contiguous slab line (x-line) to / from registers
 template <int N>
