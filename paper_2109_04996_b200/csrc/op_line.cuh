@@ -1,6 +1,6 @@
 // K1 (line kernel): fused operator  y = G^T B^T D B G x  for the interpolating
-// bases (BP1-BP4, q = p+2 Gauss points) and for the collocated sizes that have
-// no tensor-core or pencil path (p >= 10).
+// bases (BP1-BP4, q = p+2 Gauss points), one-component collocated p != 7 (BP5)
+// and three-component p >= 10 / p = 3 (BP6).
 //
 // Every 1-D contraction is a register "line": one thread loads the Q (or P)
 // values of one line of the element's slab and applies the 1-D matrix in
@@ -12,12 +12,13 @@
 //   1  x-interp  thread (j,k) gathers its node x-line straight from global
 //      memory (software-pipelined one element ahead) -> S0 [k][j][qi]
 //   2  y-interp  thread (qi,k)                        -> S1 [k][qj][qi]
-//   3  z-interp  thread (qi,qj): u_q column in registers, -> S2, and the
-//      z-derivative of it (registers)
+//   3  z-interp  thread (qi,qj): u_q column in registers, -> S2, and (q <= 10)
+//      the z-derivative of it in registers
 //   4  x / y derivatives of S2 (thread (a,b) owns one x-line and one y-line)
 //   5  QFunction per column, geometric factors loaded directly from global
 //      memory (L2-prefetched one element ahead with cp.async.bulk.prefetch),
-//      v0 / v1 in place, v2 in registers; p.(A p) as grad u . S grad u
+//      v0 / v1 in place, v2 in registers (q > 10: z-derivative recomputed here
+//      from the S2 column, v2 back into S2); p.(A p) as grad u . S grad u
 //   6  x^T / y^T derivatives in place
 //   7  column: sum of the three, z^T interp               -> S2 [c][qj][qi]
 //   8  y^T interp thread (qi,c)                         -> S1 [c][j][qi]
