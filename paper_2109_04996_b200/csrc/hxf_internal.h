@@ -23,6 +23,7 @@ struct PcgState {
   double rho, pap, alpha, beta, norm_b, target, res, tol;
   double alpha_prev;  // alpha of the previous iteration (x updates batched in pairs)
   int it, stop, converged, error, limit, fixed;
+  int stop_update;  // iteration whose update kernel stopped the solve (pAp check), 0 = none
   unsigned int counter[4];  // last-block counters: K1, update, direction, init
 };
 

@@ -34,6 +34,10 @@
 // BP5 p=11 K1 363 -> 261 us and BP3 p=15 574 -> 505 us with the late form)
 // threads per CTA targeted for q <= 4 (several elements per CTA; measured 64 ahead
 // of 128 by 2-8 % for q = 2..4 and of 256 by 5-15 %), 128 for q = 5..7
+// staged geometric factors up to this many KB per CTA step (0: always global)
+#ifndef HXF_LINE_QSMEM_MAXKB
+#define HXF_LINE_QSMEM_MAXKB 40
+#endif
 #ifndef HXF_LINE_SMALL_NT
 #define HXF_LINE_SMALL_NT 64
 #endif
@@ -91,7 +95,15 @@ struct LineTraits {
   static constexpr int OFF_EDF = OFF_EBT + ((P + 1) / 2) * eo_row_stride(Q);    // D   (Q x Q)
   static constexpr int OFF_EDT = OFF_EDF + ((Q + 1) / 2) * eo_row_stride(Q);    // D^T (Q x Q)
   static constexpr int OFF_S = round_up(OFF_EDT + ((Q + 1) / 2) * eo_row_stride(Q), 2);
-  static constexpr int SMEM_BYTES = (OFF_S + EPB * 3 * SLAB) * 8;
+  // diffusion, one component, factors of a step small enough: stage them in
+  // shared memory with one bulk async copy per step (TMA engine), refilled
+  // right after the QFunction consumed them, instead of per-point global loads
+  // (measured, K1 at 1e7 DOFs: BP5 p = 4, 5, 6, 8 -13..14 %, BP3 p = 3, 4, 5, 7
+  // -2..5 %; q <= 4 and BP3 p = 6 lose 2..8 % and keep the global loads)
+  static constexpr bool QS = DIFF && NC == 1 && Q >= 5 && !(INTERP_ && Q == 8) &&
+                             EPB * QDS * 8 <= HXF_LINE_QSMEM_MAXKB * 1024;
+  static constexpr int OFF_QS = round_up(OFF_S + EPB * 3 * SLAB, 2);
+  static constexpr int SMEM_BYTES = (OFF_QS + (QS ? EPB * QDS : 0)) * 8;
   __device__ static __forceinline__ int off(int k, int j, int i) { return (k * Q + j) * RS + i; }
 };
 
@@ -172,6 +184,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
   constexpr int P = T::P, Q = T::Q, NC = T::NC, QQ = T::QQ, Q3 = T::Q3;
   constexpr int EPB = T::EPB, NT = T::NT;
   extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t qbar;
   __shared__ double red_scratch[NT / 32 + 1];
   if (prm.stop && *prm.stop) return;
 
@@ -280,19 +293,44 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
       }
     }
   };
-  if (tid == 0) prefetch_qd(blockIdx.x);
+  // staged factors (T::QS): one bulk copy per step into smem + OFF_QS
+  auto issue_qs = [&](int64_t step) {
+    const int64_t k0 = step * EPB;
+    const int ne = (int)((prm.E - k0) < EPB ? (prm.E - k0) : EPB);
+    mbar_arrive_expect_tx(&qbar, (uint32_t)(ne * T::QDS * 8));
+    if (prm.elist) {
+      for (int i = 0; i < ne; ++i)
+        bulk_g2s(smem + T::OFF_QS + i * T::QDS, prm.qd + elem_of(k0 + i) * T::QDS,
+                 (uint32_t)(T::QDS * 8), &qbar, l2_evict_first_policy());
+    } else {
+      bulk_g2s(smem + T::OFF_QS, prm.qd + k0 * T::QDS, (uint32_t)(ne * T::QDS * 8), &qbar,
+               l2_evict_first_policy());
+    }
+  };
+  if constexpr (T::QS) {
+    if (tid == 0) {
+      mbar_init(&qbar, 1);
+      fence_mbar_init();
+      if ((int64_t)blockIdx.x < nsteps) issue_qs(blockIdx.x);
+    }
+    __syncthreads();  // mbarrier init visible
+  } else {
+    if (tid == 0) prefetch_qd(blockIdx.x);
+  }
 
   LineGeo gcur = geometry(blockIdx.x);
   double xn[P];
   load_line(gcur, 0, xn);
 
   double dot_acc = 0.0;
+  int it = 0;
 #pragma unroll 1
-  for (int64_t step = blockIdx.x; step < nsteps; step += G) {
+  for (int64_t step = blockIdx.x; step < nsteps; step += G, ++it) {
     const int64_t ks = step * EPB + slot;
     const bool eactive = aslot && ks < prm.E;
-    const double* qd_el = prm.qd + (eactive ? elem_of(ks) : 0) * T::QDS;
-    if (tid == 0) prefetch_qd(step + G);
+    const double* qd_el = T::QS ? smem + T::OFF_QS + (aslot ? slot : 0) * T::QDS
+                                : prm.qd + (eactive ? elem_of(ks) : 0) * T::QDS;
+    if (!T::QS && tid == 0) prefetch_qd(step + G);
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       double* yc = prm.y + c * prm.n_L;
@@ -357,6 +395,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         __syncthreads();
         // ---- 5: z-derivative of the column (still in S2) + QFunction
         //      (qfunction.cpp:135-162); v2 replaces the column in S2 ----
+        if constexpr (T::QS) mbar_wait(&qbar, (uint32_t)(it & 1));
         if (aslot) {
           double ln[T::EARLY ? 1 : Q];
           if constexpr (!T::EARLY) {
@@ -380,12 +419,21 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             const double a0 = S0[sp], a1 = S1[sp];
             double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
             if (eactive) {
-              s00 = ld_stream(qd_el + 0 * Q3 + pt);
-              s01 = ld_stream(qd_el + 1 * Q3 + pt);
-              s02 = ld_stream(qd_el + 2 * Q3 + pt);
-              s11 = ld_stream(qd_el + 3 * Q3 + pt);
-              s12 = ld_stream(qd_el + 4 * Q3 + pt);
-              s22 = ld_stream(qd_el + 5 * Q3 + pt);
+              if constexpr (T::QS) {
+                s00 = qd_el[0 * Q3 + pt];
+                s01 = qd_el[1 * Q3 + pt];
+                s02 = qd_el[2 * Q3 + pt];
+                s11 = qd_el[3 * Q3 + pt];
+                s12 = qd_el[4 * Q3 + pt];
+                s22 = qd_el[5 * Q3 + pt];
+              } else {
+                s00 = ld_stream(qd_el + 0 * Q3 + pt);
+                s01 = ld_stream(qd_el + 1 * Q3 + pt);
+                s02 = ld_stream(qd_el + 2 * Q3 + pt);
+                s11 = ld_stream(qd_el + 3 * Q3 + pt);
+                s12 = ld_stream(qd_el + 4 * Q3 + pt);
+                s22 = ld_stream(qd_el + 5 * Q3 + pt);
+              }
             }
             const double v0 = s00 * a0 + s01 * a1 + s02 * a2;
             const double v1 = s01 * a0 + s11 * a1 + s12 * a2;
@@ -399,7 +447,11 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             energy += a0 * v0 + a1 * v1 + a2 * v2;
           }
         }
+        if constexpr (T::QS) fence_proxy_async_smem();  // factor reads before the refill
         __syncthreads();
+        if constexpr (T::QS) {
+          if (tid == 0 && step + G < nsteps) issue_qs(step + G);
+        }
         // ---- 6: x^T and y^T derivatives in place ----
         if (aslot) {
           line_pair<T>(eDT, S0, S1, S0, S1, qa, qb);

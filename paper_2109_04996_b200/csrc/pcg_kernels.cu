@@ -102,6 +102,7 @@ __global__ void pcg_init_finalize(PcgState* st, double* hist) {
   st->converged = 0;
   st->error = 0;
   st->stop = 0;
+  st->stop_update = 0;
   if (!isfinite(norm_b)) {
     st->error = PCG_ERR_RHS;
     st->stop = 1;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(VT, OWN ? 3 : 4)
       if (!isfinite(pap)) st->error = PCG_ERR_APPLY_NAN;
       else if (rho == 0.0) st->converged = 1;
       else st->error = PCG_ERR_INDEFINITE;
+      st->stop_update = it;
       st->stop = 1;
     }
     return;
@@ -232,7 +234,9 @@ __global__ void __launch_bounds__(VT, 4)
   if (st->stop) {
     // stopped by the update kernel (pAp check, pcg.cpp:74-82): x gets only the
     // update still pending from the previous iteration (batched mode)
-    if (xmode == 2 && !st->error) {
+    // (only when this iteration's update stopped: kernels of iterations
+    // enqueued past an earlier stop must leave x alone)
+    if (xmode == 2 && !st->error && st->stop_update == it) {
       const double ap = st->alpha_prev;
       const int64_t n = n_L * m, stride = (int64_t)gridDim.x * VT;
       for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += stride)
