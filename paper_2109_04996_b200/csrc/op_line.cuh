@@ -34,7 +34,8 @@
 // BP5 p=11 K1 363 -> 261 us and BP3 p=15 574 -> 505 us with the late form)
 // threads per CTA targeted for q <= 4 (several elements per CTA; measured 64 ahead
 // of 128 by 2-8 % for q = 2..4 and of 256 by 5-15 %), 128 for q = 5..7
-// staged geometric factors up to this many KB per CTA step (0: always global)
+// staged geometric factors up to this many KB per CTA step (0: always global;
+// measured 72: BP5 p=10 -9 % but BP5 p=9 / BP3 p=8 +5..6 %)
 #ifndef HXF_LINE_QSMEM_MAXKB
 #define HXF_LINE_QSMEM_MAXKB 40
 #endif
