@@ -195,8 +195,8 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
     // for BP6 p = 2, 4, 5, 8, 9); one component: the line kernel wins at every p != 7
     // (BP5 1e7 DOFs, K1 roof line / pencil: p=1 0.55/0.48, p=3 0.76/0.54,
     // p=6 0.54/0.49, p=8 0.57/0.46, p=9 0.51/0.46, p=2,4,5 within 3 %)
-    // (p = 3: the line kernel, K1 263 vs 350 us at 1e7 DOFs)
-    if (qk == 1 && NC == 3 && P != 4 && use_pencil<P, 3>() && !pencil_disabled() &&
+    // (p = 3, 4: the line kernel, K1 263 vs 350 and 257 vs 283 us at 1e7 DOFs)
+    if (qk == 1 && NC == 3 && P != 4 && P != 5 && use_pencil<P, 3>() && !pencil_disabled() &&
         centro_symmetric(P, Q, false, B, D))
       return run_pencil_gm<P, 3>(prm, D, s, g);
   }

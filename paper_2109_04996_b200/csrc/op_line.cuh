@@ -101,7 +101,7 @@ struct LineTraits {
   // right after the QFunction consumed them, instead of per-point global loads
   // (measured, K1 at 1e7 DOFs: BP5 p = 4, 5, 6, 8 -13..14 %, BP3 p = 3, 4, 5, 7
   // -2..5 %; q <= 4 and BP3 p = 6 lose 2..8 % and keep the global loads)
-  static constexpr bool QS = DIFF && NC == 1 && Q >= 5 && !(INTERP_ && Q == 8) &&
+  static constexpr bool QS = DIFF && Q >= 5 && !(INTERP_ && Q == 8) &&
                              EPB * QDS * 8 <= HXF_LINE_QSMEM_MAXKB * 1024;
   static constexpr int OFF_QS = round_up(OFF_S + EPB * 3 * SLAB, 2);
   static constexpr int SMEM_BYTES = (OFF_QS + (QS ? EPB * QDS : 0)) * 8;
@@ -396,7 +396,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         __syncthreads();
         // ---- 5: z-derivative of the column (still in S2) + QFunction
         //      (qfunction.cpp:135-162); v2 replaces the column in S2 ----
-        if constexpr (T::QS) mbar_wait(&qbar, (uint32_t)(it & 1));
+        if constexpr (T::QS) {
+          if (c == 0) mbar_wait(&qbar, (uint32_t)(it & 1));  // once per element step
+        }
         if (aslot) {
           double ln[T::EARLY ? 1 : Q];
           if constexpr (!T::EARLY) {
@@ -448,10 +450,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             energy += a0 * v0 + a1 * v1 + a2 * v2;
           }
         }
-        if constexpr (T::QS) fence_proxy_async_smem();  // factor reads before the refill
-        __syncthreads();
         if constexpr (T::QS) {
-          if (tid == 0 && step + G < nsteps) issue_qs(step + G);
+          if (c == NC - 1) fence_proxy_async_smem();  // factor reads before the refill
+        }
+        __syncthreads();
+        if constexpr (T::QS) {  // refill after the last component's QFunction
+          if (c == NC - 1 && tid == 0 && step + G < nsteps) issue_qs(step + G);
         }
         // ---- 6: x^T and y^T derivatives in place ----
         if (aslot) {
