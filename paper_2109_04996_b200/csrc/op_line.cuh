@@ -36,6 +36,10 @@
 // of 128 by 2-8 % for q = 2..4 and of 256 by 5-15 %), 128 for q = 5..7
 // staged geometric factors up to this many KB per CTA step (0: always global;
 // measured 72: BP5 p=10 -9 % but BP5 p=9 / BP3 p=8 +5..6 %)
+// (three components: 112 measured mixed for BP6 p = 10-15, -12..+18 %)
+#ifndef HXF_LINE_QSMEM_MAXKB3
+#define HXF_LINE_QSMEM_MAXKB3 40
+#endif
 #ifndef HXF_LINE_QSMEM_MAXKB
 #define HXF_LINE_QSMEM_MAXKB 40
 #endif
@@ -102,7 +106,7 @@ struct LineTraits {
   // (measured, K1 at 1e7 DOFs: BP5 p = 4, 5, 6, 8 -13..14 %, BP3 p = 3, 4, 5, 7
   // -2..5 %; q <= 4 and BP3 p = 6 lose 2..8 % and keep the global loads)
   static constexpr bool QS = DIFF && Q >= 5 && !(INTERP_ && Q == 8) &&
-                             EPB * QDS * 8 <= HXF_LINE_QSMEM_MAXKB * 1024;
+                             EPB * QDS * 8 <= (NC == 3 ? HXF_LINE_QSMEM_MAXKB3 : HXF_LINE_QSMEM_MAXKB) * 1024;
   static constexpr int OFF_QS = round_up(OFF_S + EPB * 3 * SLAB, 2);
   static constexpr int SMEM_BYTES = (OFF_QS + (QS ? EPB * QDS : 0)) * 8;
   __device__ static __forceinline__ int off(int k, int j, int i) { return (k * Q + j) * RS + i; }
