@@ -1,3 +1,6 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$? >> gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 400 python bench.py > gpurun_out/bench.log 2>&1
 timeout 2400 python tools/sweep.py --bp bp5 --p 1-15 --sizes 1e5,1e6,1e7,3e7 --cpu --out gpurun_out/fs_bp5.md --csv gpurun_out/fs_bp5.csv --records gpurun_out/fs_bp5.jsonl > gpurun_out/fs_bp5.log 2>&1
 timeout 1200 python tools/sweep.py --bp bp3 --p 1-15 --sizes 1e7 --out gpurun_out/fs_bp3.md > gpurun_out/fs_bp3.log 2>&1
 timeout 600 python tools/sweep.py --bp bp3 --p 7 --dims 31 --cpu --out gpurun_out/fs_bp3_c2.md > gpurun_out/fs_bp3_c2.log 2>&1
