@@ -96,7 +96,9 @@ def test_pcg_iterations_and_solution(ctx, name):
     x, rep = op.pcg(g["rhs"], diag, tol=float(g["tol"]))
     assert abs(rep["iterations"] - int(g["iterations"])) <= 1
     assert rep["converged"] == bool(g["converged"])
-    assert oracle.rel_max_diff(g["solution"], x) <= 1e-8
+    # same iterations and (FMA / RED rounding aside) the same iterates: measured
+    # <= 1e-13 on every fixture (a missed or doubled x update shows at ~1e-8)
+    assert oracle.rel_max_diff(g["solution"], x) <= 1e-11
     assert abs(rep["residual_history"][0] - g["history"][0]) <= 1e-14 * g["history"][0]
 
 
