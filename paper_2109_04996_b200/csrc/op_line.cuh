@@ -105,7 +105,8 @@ struct LineTraits {
   // right after the QFunction consumed them, instead of per-point global loads
   // (measured, K1 at 1e7 DOFs: BP5 p = 4, 5, 6, 8 -13..14 %, BP3 p = 3, 4, 5, 7
   // -2..5 %; q <= 4 and BP3 p = 6 lose 2..8 % and keep the global loads)
-  static constexpr bool QS = DIFF && Q >= 5 && !(INTERP_ && Q == 8) &&
+  // (mass: interpolating bases only, where a barrier follows the QFunction)
+  static constexpr bool QS = (DIFF || INTERP_) && Q >= 5 && !(INTERP_ && Q == 8) &&
                              EPB * QDS * 8 <= (NC == 3 ? HXF_LINE_QSMEM_MAXKB3 : HXF_LINE_QSMEM_MAXKB) * 1024;
   static constexpr int OFF_QS = round_up(OFF_S + EPB * 3 * SLAB, 2);
   static constexpr int SMEM_BYTES = (OFF_QS + (QS ? EPB * QDS : 0)) * 8;
@@ -485,10 +486,13 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
         }
       } else {
         // mass QFunction (qfunction.cpp:124-133), column-local
+        if constexpr (T::QS) {
+          if (c == 0) mbar_wait(&qbar, (uint32_t)(it & 1));
+        }
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
           const int pt = k * QQ + qb * Q + qa;
-          const double m = eactive ? ld_stream(qd_el + pt) : 0.0;
+          const double m = eactive ? (T::QS ? qd_el[pt] : ld_stream(qd_el + pt)) : 0.0;
           w[k] = m * uq[k];
           energy += uq[k] * w[k];
         }
@@ -503,7 +507,13 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
 #pragma unroll
           for (int k = 0; k < P; ++k) S2[T::off(k, qb, qa)] = t[k];
         }
+        if constexpr (T::QS && !T::DIFF) {
+          if (c == NC - 1) fence_proxy_async_smem();  // mass factor reads before the refill
+        }
         __syncthreads();
+        if constexpr (T::QS && !T::DIFF) {
+          if (c == NC - 1 && tid == 0 && step + G < nsteps) issue_qs(step + G);
+        }
         // ---- 8: y^T interp, line (qi, k) -> S1 [k][j][qi] ----
         if (aslot && l < Q * P) {
           double ln[Q], t[P];
