@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
           const double yk0 = prm.coef * (y01[kk][0] + z2.x);
           const double yk1 = prm.coef * (y01[kk][1] + z2.y);
           if (!(prm.ablate & 2)) {
-            if (!((gcur.cmask >> (2 * kk)) & 1u)) red_add(yc + node_of(gcur, kk, 0), yk0);
-            if (!((gcur.cmask >> (2 * kk + 1)) & 1u)) red_add(yc + node_of(gcur, kk, 1), yk1);
+            red_add_if(yc + node_of(gcur, kk, 0), yk0, !((gcur.cmask >> (2 * kk)) & 1u));
+            red_add_if(yc + node_of(gcur, kk, 1), yk1, !((gcur.cmask >> (2 * kk + 1)) & 1u));
           }
         }
       }
