@@ -44,10 +44,16 @@ struct PencilTraits {
   static constexpr int EPB = PP >= 64 ? 1 : (PP == 25 ? 5 : (PP == 36 ? 3 : (PP == 49 ? 2 : 64 / PP)));
   static constexpr int NT = pencil_round_up(EPB * PP, 32);
   static constexpr bool SWZ = (P == 8);  // XOR-rotated 64-byte rows
-  static constexpr int RS = SWZ ? 8 : pencil_row_stride(P);
+  // p != 7: layout searched for the fewest shared-memory wavefronts over the
+  // kernel's three access patterns (x-line rows, y-columns, z-lines; scalar
+  // 8-byte accesses, 34 % bank conflicts with the 16-byte aligned layout at
+  // p = 8): RS = P and a plane stride PL_SEARCH; other P keep the aligned rows
+  static constexpr int PL_SEARCH = P == 6 ? 37 : (P == 9 ? 81 : 0);  // (P = 10: measured +2.5 %)
+  static constexpr bool VROW = SWZ || PL_SEARCH == 0;  // 16-byte row chunks (LDS.128)
+  static constexpr int RS = SWZ ? 8 : (VROW ? pencil_row_stride(P) : P);
   // plane stride: padded layouts skew consecutive planes by 16 banks (+64 B);
   // the swizzled p = 7 layout flips the row parity per plane instead (no pad)
-  static constexpr int PL = SWZ ? P * RS : P * RS + 8;
+  static constexpr int PL = SWZ ? P * RS : (VROW ? P * RS + 8 : PL_SEARCH);
   static constexpr int SLAB = P * PL;    // doubles per element slab
   static constexpr int QDS = 6 * P3;     // geometric factors per element (even)
   static constexpr int DR = pencil_round_up(P, 2);  // matrix row stride (16-byte rows)
@@ -224,23 +230,33 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       // ---- F: D along x (-> C) and y (-> B) from slab A, one D row per two pencils ----
       if (active_slot) {
         double row[P], col[P];
+        if constexpr (T::VROW) {
 #pragma unroll
-        for (int a = 0; a + 1 < P; a += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(SA + T::chunk(lb, la, a / 2));
-          row[a] = v.x;
-          row[a + 1] = v.y;
+          for (int a = 0; a + 1 < P; a += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(SA + T::chunk(lb, la, a / 2));
+            row[a] = v.x;
+            row[a + 1] = v.y;
+          }
+          if (P & 1) row[P - 1] = SA[T::off(lb, la, P - 1)];
+        } else {
+#pragma unroll
+          for (int a = 0; a < P; ++a) row[a] = SA[T::off(lb, la, a)];
         }
-        if (P & 1) row[P - 1] = SA[T::off(lb, la, P - 1)];
 #pragma unroll
         for (int b = 0; b < P; ++b) col[b] = SA[T::off(lb, b, la)];
         double gx[P], gy[P];
         eo_pair<P, -1>(eD, row, col, gx, gy);
 #pragma unroll
         for (int o = 0; o < P; ++o) SB[T::off(lb, o, la)] = gy[o];
+        if constexpr (T::VROW) {
 #pragma unroll
-        for (int a = 0; a + 1 < P; a += 2)
-          *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(gx[a], gx[a + 1]);
-        if (P & 1) SC[T::off(lb, la, P - 1)] = gx[P - 1];
+          for (int a = 0; a + 1 < P; a += 2)
+            *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(gx[a], gx[a + 1]);
+          if (P & 1) SC[T::off(lb, la, P - 1)] = gx[P - 1];
+        } else {
+#pragma unroll
+          for (int a = 0; a < P; ++a) SC[T::off(lb, la, a)] = gx[a];
+        }
       }
       if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
       __syncthreads();
@@ -293,23 +309,33 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       // ---- T: D^T along x (C, in place) and y (B, in place) ----
       if (active_slot) {
         double row[P], col[P];
+        if constexpr (T::VROW) {
 #pragma unroll
-        for (int a = 0; a + 1 < P; a += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(SC + T::chunk(lb, la, a / 2));
-          row[a] = v.x;
-          row[a + 1] = v.y;
+          for (int a = 0; a + 1 < P; a += 2) {
+            const double2 v = *reinterpret_cast<const double2*>(SC + T::chunk(lb, la, a / 2));
+            row[a] = v.x;
+            row[a + 1] = v.y;
+          }
+          if (P & 1) row[P - 1] = SC[T::off(lb, la, P - 1)];
+        } else {
+#pragma unroll
+          for (int a = 0; a < P; ++a) row[a] = SC[T::off(lb, la, a)];
         }
-        if (P & 1) row[P - 1] = SC[T::off(lb, la, P - 1)];
 #pragma unroll
         for (int b = 0; b < P; ++b) col[b] = SB[T::off(lb, b, la)];
         double tx[P], ty[P];
         eo_pair<P, -1>(eDT, row, col, tx, ty);
 #pragma unroll
         for (int o = 0; o < P; ++o) SB[T::off(lb, o, la)] = ty[o];
+        if constexpr (T::VROW) {
 #pragma unroll
-        for (int a = 0; a + 1 < P; a += 2)
-          *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(tx[a], tx[a + 1]);
-        if (P & 1) SC[T::off(lb, la, P - 1)] = tx[P - 1];
+          for (int a = 0; a + 1 < P; a += 2)
+            *reinterpret_cast<double2*>(SC + T::chunk(lb, la, a / 2)) = make_double2(tx[a], tx[a + 1]);
+          if (P & 1) SC[T::off(lb, la, P - 1)] = tx[P - 1];
+        } else {
+#pragma unroll
+          for (int a = 0; a < P; ++a) SC[T::off(lb, la, a)] = tx[a];
+        }
       }
       __syncthreads();
 
