@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
       // ---- P: z-line of A, next item's gather into A, D along z + QFunction ----
       double u[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) u[k] = SA[T::off(k, lb, la)];
+      for (int k = 0; k < P; ++k) u[k] = active_slot ? SA[T::off(k, lb, la)] : 0.0;
       store_line(gpf, xn);  // item q+1's masked z-line (this thread's column only)
       gpf = ((q + 2) / NC == (q + 1) / NC && NC > 1) ? gpf : geometry(item_step(q + 2));
       load_line(gpf, (q + 2) % NC, xn);  // item q+2 lands while items q, q+1 compute
@@ -277,7 +277,9 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
         const double g2 = g2v[k];
         const int sp = T::off(k, lb, la);
         const int pt = k * PP + lb * P + la;
-        const double g0 = SC[sp], g1 = SB[sp];
+        // (threads beyond the element slots read nothing: no race with the
+        // active threads' in-place writes below)
+        const double g0 = active_slot ? SC[sp] : 0.0, g1 = active_slot ? SB[sp] : 0.0;
         double s00 = 0, s01 = 0, s02 = 0, s11 = 0, s12 = 0, s22 = 0;
         if (gcur.active) {
           s00 = qd_el[0 * P3 + pt];
