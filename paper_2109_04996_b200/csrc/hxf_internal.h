@@ -56,6 +56,7 @@ struct OpParams {
   PcgAlphaFin fin;           // PCG: last-CTA alpha finalisation (fin.st == nullptr: off)
   int rev;                   // sweep elements last to first (L2 reuse across CG kernels)
   const int* elist;          // element ids to process (E entries), nullptr = 0..E-1 (DMMA kernel)
+  int pdl;                   // launch with programmatic dependent launch (single apply)
   int cons_store;            // DMMA kernel: store y = x on the constrained rows it gathers
                              // (y zero-filled by the caller instead of preset by init_y)
 };
@@ -108,7 +109,8 @@ int num_sms();
 // "generic" -> 2 (op_kernel.cuh only).
 int op_kernel_choice();
 bool pencil_disabled();
-bool dmma_pad_disabled();     // HXF_DMMA_PAD=0: p = 4..6 back on the pencil kernel (A/B)
+bool dmma_pad_disabled();
+bool pdl_apply_disabled();    // HXF_PDL_APPLY=0: single apply without PDL (A/B)     // HXF_DMMA_PAD=0: p = 4..6 back on the pencil kernel (A/B)
 bool pdl_enabled();           // HXF_PDL=1: programmatic dependent launch (off by default)
 bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward
 int dmma_stages();
@@ -121,8 +123,8 @@ void count_launch(int n = 1);
 // while its predecessor drains; it must pdl_wait() before touching anything
 // the predecessor writes.  Only for single-wave grids that also pdl_trigger().
 template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                       cudaStream_t s, Args&&... args) {
+cudaError_t launch_pdl_if(bool allow, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -130,10 +132,16 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = allow ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  return launch_pdl_if(pdl_enabled(), kern, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 }  // namespace hxf

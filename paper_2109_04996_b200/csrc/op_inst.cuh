@@ -129,7 +129,8 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   const int grid = (int)(prm.E < max_ctas ? prm.E : max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
-  const cudaError_t err = launch_pdl(kern, dim3(grid), dim3(T::NT), T::SMEM_BYTES, s, prm);
+  const cudaError_t err = launch_pdl_if(pdl_enabled() || prm.pdl, kern, dim3(grid), dim3(T::NT),
+                                        T::SMEM_BYTES, s, prm);
   count_launch();
   return err;
 }
