@@ -46,6 +46,10 @@
 #ifndef HXF_LINE_SMALL_NT
 #define HXF_LINE_SMALL_NT 64
 #endif
+// late-form QFunction unroll (measured 4: -7..+11 % across q = 11-16, kept 2)
+#ifndef HXF_LINE_QF_UNROLL
+#define HXF_LINE_QF_UNROLL 2
+#endif
 #ifndef HXF_LINE_EARLY_Q
 #define HXF_LINE_EARLY_Q 10
 #endif
@@ -66,6 +70,7 @@ struct LineTraits {
   // z-derivative / v2 of the column kept in registers across phases 4-7
   // (measured faster at q = 9); larger q recompute it from S2 in phase 5
   static constexpr bool EARLY = Q <= HXF_LINE_EARLY_Q;
+  static constexpr int QFU = HXF_LINE_QF_UNROLL;  // late-form QFunction unroll
   static constexpr bool INTERP = INTERP_;
   static constexpr bool DIFF = QK == 1;  // one qdata kind per launch (1 diffusion, 2 mass)
   static constexpr int QQ = Q * Q, Q3 = Q * Q * Q, P3 = P * P * P;
@@ -411,7 +416,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB)
             for (int k = 0; k < Q; ++k) ln[k] = S2[T::off(k, qb, qa)];
           }
           // (late form: partial unroll, two points' factors in flight)
-#pragma unroll (T::EARLY ? Q : 2)
+#pragma unroll (T::EARLY ? Q : T::QFU)
           for (int k = 0; k < Q; ++k) {
             const int sp = T::off(k, qb, qa);
             const int pt = k * QQ + qb * Q + qa;
