@@ -48,6 +48,12 @@ const char* hxf_last_error(void);
 int hxf_abi_version(void);
 /* Number of hxf kernels launched so far in this process (instrumentation). */
 int64_t hxf_launch_count(void);
+/* Test knob: cap the grid of the operator and PCG vector kernels at `cap`
+ * CTAs (0 = no cap; initial value from the HXF_MAX_GRID environment
+ * variable), so small meshes exercise the multi-element-per-CTA loops the
+ * full-size configurations run.  Returns the previous cap.  Affects launches
+ * made (and graphs captured) after the call. */
+int hxf_debug_set_grid_cap(int cap);
 
 /* ---- context: one CUDA device (+ optional NCCL communicator) ----------- */
 int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out);
@@ -132,6 +138,47 @@ int hxf_qdata_compute(hxf_ctx* ctx, int p, int q, const double* interp1d, const 
                       const double* qweights, int64_t num_elements, int64_t n_L,
                       const double* coords, const int64_t* indices, const int dims[3],
                       hxf_qdata_kind kind, double* out, hxf_memspace space);
+
+/* ---- standalone element restriction: replaces ElemRestriction ----------------
+ * proj/include/hexfem/restriction.hpp:14-50 (make_restriction, apply_g,
+ * apply_g_transpose, multiplicity, gather_scalar).  indices = E x (p+1)^3
+ * int64 (verified entry by entry against the structured box, then not stored)
+ * or NULL with dims set.  Lengths are the span sizes the reference checks;
+ * a mismatch is HXF_EINVAL with the reference's message.  G^T accumulates in
+ * the reference's colour-class order (bitwise equal) on the structured box. */
+typedef struct hxf_restr hxf_restr;
+int hxf_elem_restriction_create(hxf_ctx* ctx, int p, int m, int64_t num_elements, int64_t n_L,
+                                const int64_t* indices, const int dims[3], hxf_restr** out);
+int hxf_elem_restriction_destroy(hxf_restr* r);
+int hxf_elem_restriction_is_structured(const hxf_restr* r);
+/* transpose = 0: apply_g (in = m*n_L L-vector, out = m*E*S E-vector);
+ * transpose = 1: apply_g_transpose (in = E-vector, out = L-vector, overwritten). */
+int hxf_elem_restriction_apply(hxf_restr* r, int transpose, const double* in, int64_t in_len,
+                               double* out, int64_t out_len, hxf_memspace space);
+int hxf_elem_restriction_multiplicity(hxf_restr* r, double* out, int64_t out_len,
+                                      hxf_memspace space);
+/* gather_scalar (restriction.cpp:86-106): single-component G^T of E*S values. */
+int hxf_elem_restriction_gather_scalar(hxf_restr* r, const double* e_scalar, int64_t e_len,
+                                       double* l_scalar, int64_t l_len, hxf_memspace space);
+
+/* ---- contraction kernels (contraction.hpp:43-75) ------------------------- */
+/* contract_batch (contraction.cpp:177-206): the 1-D matrix (n_out x n_in
+ * row-major, HOST) applied along tensor dimension dim of ne element blocks
+ * of shape in_shape (x fastest); accumulate != 0 adds into out.  flops (or
+ * NULL) is incremented by 2 per multiply-add like the reference's
+ * FlopCounter.  Bitwise equal to the reference's sum-factorized path. */
+int hxf_contract_batch(hxf_ctx* ctx, const double* matrix, int64_t matrix_len, int n_out,
+                       int n_in, int dim, const int in_shape[3], int64_t ne, const double* in,
+                       int64_t in_len, double* out, int64_t out_len, int accumulate,
+                       hxf_memspace space, uint64_t* flops);
+/* apply_tensor_3d (tensor_basis.hpp:38-47, tensor_basis.cpp:73-99): one
+ * element, m components stored consecutively. */
+int hxf_apply_tensor_3d(hxf_ctx* ctx, int p, int q, const double* interp1d, const double* grad1d,
+                        hxf_eval_mode mode, hxf_eval_dir dir, int m, const double* u,
+                        int64_t u_len, double* v, int64_t v_len, hxf_memspace space);
+/* flops_estimate (contraction.cpp:334-340): multiply-adds x 2 per element of
+ * the sum-factorized kernel; Grad = 3 x Interp; direction-independent. */
+uint64_t hxf_flops_estimate(int p, int q, int m, hxf_eval_mode mode);
 
 /* ---- PCG: replaces pcg(ApplyFn, ...) for this operator ---------------------
  * proj/include/hexfem/pcg.hpp:13-41, proj/src/pcg.cpp:24-115.  x0 = 0;

@@ -87,6 +87,14 @@ def _lib(impl: str) -> C.CDLL:
     L.orc_quadrature.argtypes = [I, I, pd, pd]
     L.orc_basis.argtypes = [I, I, I, pd, pd]
     L.orc_apply_basis.argtypes = [I, I, I, I, I, I64, pd, I64, pd, I64]
+    U64 = C.c_uint64
+    L.orc_contract_batch.argtypes = [pd, I64, I, I, I, pi, I64, pd, I64, pd, I64, I,
+                                     C.POINTER(U64)]
+    L.orc_apply_tensor_3d.argtypes = [I, I, I, I, I, I, pd, I64, pd, I64]
+    L.orc_flops_estimate.restype = U64
+    L.orc_flops_estimate.argtypes = [I, I, I, I]
+    L.orc_apply_basis_counted.argtypes = [I, I, I, I, I, I64, pd, I64, pd, I64, C.POINTER(U64)]
+    L.orc_gather_scalar.argtypes = [P, pd, I64, pd, I64]
     if impl == "reference":
         L.orc_run_bench.argtypes = [I, I, I, I, I, I, I, I, pd]
         L.orc_sweep_model.argtypes = [I, I, pi, I, pi, I, I, D, D, C.c_char_p, I64, pd]
@@ -140,6 +148,57 @@ def apply_basis(p: int, kind: str, q: int, mode: str, direction: str, ne: int,
     _check(L, L.orc_apply_basis(p, _kind(kind), q, int(grad), int(tr), ne, _dp(u), u.size,
                                 _dp(out), out.size))
     return out
+
+
+def contract_batch(matrix, n_out: int, n_in: int, dim: int, shape, ne: int, u,
+                   out=None, accumulate: bool = False, impl: str = "oracle"):
+    """contract_batch (src/contraction.cpp:177-206) -> (out, flops counted)."""
+    L = _lib(impl)
+    M = np.ascontiguousarray(matrix, dtype=np.float64).reshape(-1)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    in_elem = int(shape[0]) * int(shape[1]) * int(shape[2])
+    n = ne * (in_elem // max(n_in, 1)) * n_out if n_in > 0 else 0
+    out = np.zeros(n) if out is None else np.array(out, dtype=np.float64, copy=True)
+    sh = np.ascontiguousarray(shape, dtype=np.int32)
+    cnt = C.c_uint64(0)
+    _check(L, L.orc_contract_batch(_dp(M), M.size, n_out, n_in, dim,
+                                   sh.ctypes.data_as(C.POINTER(C.c_int)), ne, _dp(u), u.size,
+                                   _dp(out), out.size, int(bool(accumulate)), C.byref(cnt)))
+    return out, int(cnt.value)
+
+
+def apply_tensor_3d(p: int, kind: str, q: int, mode: str, direction: str, m: int, u,
+                    impl: str = "oracle") -> np.ndarray:
+    """apply_tensor_3d (src/tensor_basis.cpp:73-99)."""
+    L = _lib(impl)
+    grad, tr = mode == "grad", direction == "transpose"
+    nd3, nq3 = (p + 1) ** 3, q ** 3
+    out_e = nd3 if tr else (3 * nq3 if grad else nq3)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(m * out_e)
+    _check(L, L.orc_apply_tensor_3d(p, _kind(kind), q, int(grad), int(tr), m, _dp(u), u.size,
+                                    _dp(out), out.size))
+    return out
+
+
+def flops_estimate(p: int, q: int, m: int, mode: str, impl: str = "oracle") -> int:
+    """flops_estimate (src/contraction.cpp:334-340)."""
+    return int(_lib(impl).orc_flops_estimate(p, q, m, 1 if mode == "grad" else 0))
+
+
+def apply_basis_counted(p: int, kind: str, q: int, mode: str, direction: str, ne: int, u,
+                        impl: str = "oracle"):
+    """apply_basis_batch with a FlopCounter attached -> (out, counted flops)."""
+    L = _lib(impl)
+    grad, tr = mode == "grad", direction == "transpose"
+    nd3, nq3 = (p + 1) ** 3, q ** 3
+    out_e = 3 * nq3 if (grad and not tr) else (nq3 if not tr else nd3)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(ne * out_e)
+    cnt = C.c_uint64(0)
+    _check(L, L.orc_apply_basis_counted(p, _kind(kind), q, int(grad), int(tr), ne, _dp(u), u.size,
+                                        _dp(out), out.size, C.byref(cnt)))
+    return out, int(cnt.value)
 
 
 class Problem:
@@ -245,6 +304,13 @@ class Problem:
         report = {"iterations": it.value, "converged": bool(conv.value),
                   "residual_history": hist[: it.value + 1].copy()}
         return x, report
+
+    def gather_scalar(self, e_scalar: np.ndarray) -> np.ndarray:
+        """gather_scalar (src/restriction.cpp:86-106) over this problem's restriction."""
+        e = np.ascontiguousarray(e_scalar, dtype=np.float64)
+        out = np.zeros(self.num_nodes)
+        _check(self._L, self._L.orc_gather_scalar(self._h, _dp(e), e.size, _dp(out), out.size))
+        return out
 
     def l2_error(self, u: np.ndarray) -> float:
         u = np.ascontiguousarray(u, dtype=np.float64)

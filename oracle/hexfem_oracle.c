@@ -293,6 +293,69 @@ int orc_apply_basis(int p, int kind, int q, int mode, int dir, int64_t ne, const
   return 0;
 }
 
+/* contract_batch (src/contraction.cpp:177-206): the same checks in the same
+ * order, then contract_sf element by element; 2 flops per multiply-add. */
+int orc_contract_batch(const double* M, int64_t m_len, int n_out, int n_in, int dim,
+                       const int* shape, int64_t ne, const double* in, int64_t in_len, double* out,
+                       int64_t out_len, int accumulate, uint64_t* flops) {
+  if (dim < 0 || dim > 2) return fail(1, "contract_batch: dim must be 0, 1 or 2");
+  if (n_out < 1 || n_in < 1 || shape[dim] != n_in)
+    return fail(1, "contract_batch: inconsistent shapes");
+  if (m_len != (int64_t)n_out * n_in) return fail(1, "contract_batch: matrix size mismatch");
+  const int64_t in_elem = (int64_t)shape[0] * shape[1] * shape[2];
+  const int64_t out_elem = in_elem / n_in * n_out;
+  if (in_len < ne * in_elem || out_len < ne * out_elem)
+    return fail(1, "contract_batch: buffer too small");
+  for (int64_t e = 0; e < ne; ++e)
+    contract(M, n_out, n_in, dim, shape, in + e * in_elem, out + e * out_elem, accumulate);
+  if (flops) *flops += 2 * (uint64_t)ne * (uint64_t)out_elem * (uint64_t)n_in;
+  return 0;
+}
+
+/* apply_tensor_3d (src/tensor_basis.cpp:73-99): m components stored
+ * consecutively, each an apply_basis_batch with ne = 1. */
+int orc_apply_tensor_3d(int p, int kind, int q, int mode, int dir, int m, const double* u,
+                        int64_t u_len, double* v, int64_t v_len) {
+  if (m < 1) return fail(1, "apply_tensor_3d: m must be >= 1");
+  Basis b;
+  int rc = basis_make(&b, p, kind, q);
+  if (rc) return rc;
+  const int64_t nd = (int64_t)(p + 1) * (p + 1) * (p + 1), nq = (int64_t)q * q * q;
+  const int64_t in_size = !dir ? nd : (mode ? 3 * nq : nq);
+  const int64_t out_size = !dir ? (mode ? 3 * nq : nq) : nd;
+  if (u_len != m * in_size || v_len != m * out_size) {
+    basis_free(&b);
+    return fail(1, "apply_tensor_3d: shape mismatch");
+  }
+  const int mx = (p + 1) > q ? p + 1 : q;
+  double* ta = malloc(sizeof(double) * mx * mx * mx);
+  double* tb = malloc(sizeof(double) * mx * mx * mx);
+  for (int c = 0; c < m; ++c) basis_batch(&b, mode, dir, 1, u + c * in_size, v + c * out_size, ta, tb);
+  free(ta); free(tb);
+  basis_free(&b);
+  return 0;
+}
+
+/* flops_estimate (src/contraction.cpp:334-340) */
+uint64_t orc_flops_estimate(int p, int q, int m, int mode) {
+  const uint64_t p1 = (uint64_t)p + 1, qq = (uint64_t)q;
+  const uint64_t interp = 2 * (uint64_t)m * (qq * p1 * p1 * p1 + qq * qq * p1 * p1 + qq * qq * qq * p1);
+  return mode ? 3 * interp : interp;
+}
+
+/* apply_basis_batch with a counter: chain3's three contractions per chain,
+ * counted like contract_sf<true> (one per multiply-add, 2 flops each). */
+int orc_apply_basis_counted(int p, int kind, int q, int mode, int dir, int64_t ne,
+                            const double* in, int64_t n_in, double* out, int64_t n_out,
+                            uint64_t* flops) {
+  const int rc = orc_apply_basis(p, kind, q, mode, dir, ne, in, n_in, out, n_out);
+  if (rc) return rc;
+  const uint64_t n1 = (uint64_t)p + 1, qq = (uint64_t)q;
+  const uint64_t chain = qq * n1 * n1 * n1 + qq * qq * n1 * n1 + qq * qq * qq * n1;
+  if (flops) *flops += 2 * (uint64_t)ne * chain * (mode ? 3 : 1);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ mesh
  * Structured unit-cube hex mesh, GLL lattice, optional sine bump
  * (src/mesh.cpp:12-78); element node indices (src/mesh.cpp:80-104). */
@@ -817,6 +880,15 @@ int orc_solve(void* h, double tol, int max_iter, int jacobi, int fixed_iters, do
 }
 
 /* l2_error (src/bench.cpp:139-189): Gauss q=p+2 rule regardless of the BP. */
+int orc_gather_scalar(void* h, const double* e_scalar, int64_t e_len, double* l_scalar,
+                      int64_t l_len) {
+  const Restr* r = &((Problem*)h)->op.r;
+  if (l_len != r->n_L) return fail(1, "gather_scalar: L-vector length mismatch");
+  if (e_len != r->E * r->S) return fail(1, "gather_scalar: E-vector length mismatch");
+  apply_gt(r, 1, e_scalar, l_scalar);
+  return 0;
+}
+
 double orc_l2_error(void* h, const double* u) {
   Problem* pr = h;
   const Mesh* mesh = &pr->mesh;

@@ -45,6 +45,23 @@ int orc_quadrature(int kind, int q, double* pts, double* wts);
 int orc_basis(int p, int kind, int q, double* interp, double* grad);
 int orc_apply_basis(int p, int kind, int q, int mode, int dir, int64_t ne, const double* in,
                     int64_t n_in, double* out, int64_t n_out);
+/* contract_batch (src/contraction.cpp:177-206) with the FlopCounter
+ * (*flops += 2 per multiply-add, when flops != NULL). */
+int orc_contract_batch(const double* M, int64_t m_len, int n_out, int n_in, int dim,
+                       const int* shape, int64_t ne, const double* in, int64_t in_len, double* out,
+                       int64_t out_len, int accumulate, uint64_t* flops);
+/* apply_tensor_3d (src/tensor_basis.cpp:73-99) */
+int orc_apply_tensor_3d(int p, int kind, int q, int mode, int dir, int m, const double* u,
+                        int64_t u_len, double* v, int64_t v_len);
+/* flops_estimate (src/contraction.cpp:334-340) */
+uint64_t orc_flops_estimate(int p, int q, int m, int mode);
+/* apply_basis_batch with a FlopCounter attached: the instrumented count */
+int orc_apply_basis_counted(int p, int kind, int q, int mode, int dir, int64_t ne,
+                            const double* in, int64_t n_in, double* out, int64_t n_out,
+                            uint64_t* flops);
+/* gather_scalar (src/restriction.cpp:86-106) over the problem's restriction */
+int orc_gather_scalar(void* h, const double* e_scalar, int64_t e_len, double* l_scalar,
+                      int64_t l_len);
 
 #ifdef __cplusplus
 }

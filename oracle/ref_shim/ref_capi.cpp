@@ -201,6 +201,70 @@ int orc_apply_basis(int p, int kind, int q, int mode, int dir, int64_t ne, const
   });
 }
 
+int orc_contract_batch(const double* M, int64_t m_len, int n_out, int n_in, int dim,
+                       const int* shape, int64_t ne, const double* in, int64_t in_len, double* out,
+                       int64_t out_len, int accumulate, uint64_t* flops) {
+  return guarded([&] {
+    FlopCounter counter;
+    KernelPlan plan;
+    plan.flops = flops ? &counter : nullptr;
+    contract_batch(plan, std::span<const double>(M, std::size_t(m_len)), n_out, n_in, dim,
+                   std::array<int, 3>{shape[0], shape[1], shape[2]}, ne,
+                   std::span<const double>(in, std::size_t(in_len)),
+                   std::span<double>(out, std::size_t(out_len)), accumulate != 0);
+    if (flops) *flops += counter.count();
+  });
+}
+
+int orc_apply_tensor_3d(int p, int kind, int q, int mode, int dir, int m, const double* u,
+                        int64_t u_len, double* v, int64_t v_len) {
+  return guarded([&] {
+    auto b = make_basis(p, make_quadrature(kind ? QuadratureKind::GaussLobattoLegendre
+                                                : QuadratureKind::GaussLegendre, q));
+    apply_tensor_3d(b, mode ? EvalMode::Grad : EvalMode::Interp,
+                    dir ? EvalDirection::Transpose : EvalDirection::Forward, m,
+                    std::span<const double>(u, std::size_t(u_len)),
+                    std::span<double>(v, std::size_t(v_len)));
+  });
+}
+
+uint64_t orc_flops_estimate(int p, int q, int m, int mode) {
+  KernelPlan plan;
+  plan.p = p;
+  plan.q = q;
+  plan.m = m;
+  return flops_estimate(plan, mode ? EvalMode::Grad : EvalMode::Interp);
+}
+
+int orc_apply_basis_counted(int p, int kind, int q, int mode, int dir, int64_t ne,
+                            const double* in, int64_t n_in, double* out, int64_t n_out,
+                            uint64_t* flops) {
+  return guarded([&] {
+    auto b = make_basis(p, make_quadrature(kind ? QuadratureKind::GaussLobattoLegendre
+                                                : QuadratureKind::GaussLegendre, q));
+    FlopCounter counter;
+    KernelPlan plan;
+    plan.p = p;
+    plan.q = q;
+    plan.flops = &counter;
+    ContractionScratch scratch;
+    apply_basis_batch(plan, b, mode ? EvalMode::Grad : EvalMode::Interp,
+                      dir ? EvalDirection::Transpose : EvalDirection::Forward, ne,
+                      std::span<const double>(in, std::size_t(n_in)),
+                      std::span<double>(out, std::size_t(n_out)), scratch);
+    if (flops) *flops += counter.count();
+  });
+}
+
+int orc_gather_scalar(void* h, const double* e_scalar, int64_t e_len, double* l_scalar,
+                      int64_t l_len) {
+  return guarded([&] {
+    gather_scalar(static_cast<RefProblem*>(h)->prob.op.restriction,
+                  std::span<const double>(e_scalar, std::size_t(e_len)),
+                  std::span<double>(l_scalar, std::size_t(l_len)));
+  });
+}
+
 // The reference benchmark record (bench.cpp:191-229): returns dofs_rate and
 // fills rec[] = {n, iterations, seconds, E, q}.
 int orc_run_bench(int bp, int p, int nx, int ny, int nz, int deform, int threads, int iters,

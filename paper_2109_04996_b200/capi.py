@@ -29,7 +29,11 @@ EXPORTS = (
     "hxf_comm_unique_id", "hxf_comm_create_nccl", "hxf_comm_wrap_nccl", "hxf_comm_group_create",
     "hxf_comm_group_destroy", "hxf_comm_create_group", "hxf_comm_destroy", "hxf_comm_rank",
     "hxf_comm_size", "hxf_comm_allreduce_sum", "hxf_operator_set_partition",
-    "hxf_operator_halo_sum", "hxf_pcg_host_batch",
+    "hxf_operator_halo_sum", "hxf_pcg_host_batch", "hxf_debug_set_grid_cap",
+    "hxf_elem_restriction_create", "hxf_elem_restriction_destroy",
+    "hxf_elem_restriction_is_structured", "hxf_elem_restriction_apply",
+    "hxf_elem_restriction_multiplicity", "hxf_elem_restriction_gather_scalar",
+    "hxf_contract_batch", "hxf_apply_tensor_3d", "hxf_flops_estimate",
 )
 
 
@@ -120,6 +124,18 @@ def lib() -> C.CDLL:
     L.hxf_operator_set_partition.argtypes = [P, P, C.POINTER(PartitionDesc)]
     L.hxf_operator_halo_sum.argtypes = [P, P, I]
     L.hxf_pcg_host_batch.argtypes = [P, I, P, P, C.POINTER(PcgOptions), P, P]
+    L.hxf_debug_set_grid_cap.argtypes = [I]
+    L.hxf_elem_restriction_create.argtypes = [P, I, I, I64, I64, P, P, C.POINTER(P)]
+    L.hxf_elem_restriction_destroy.argtypes = [P]
+    L.hxf_elem_restriction_is_structured.argtypes = [P]
+    L.hxf_elem_restriction_apply.argtypes = [P, I, P, I64, P, I64, I]
+    L.hxf_elem_restriction_multiplicity.argtypes = [P, P, I64, I]
+    L.hxf_elem_restriction_gather_scalar.argtypes = [P, P, I64, P, I64, I]
+    L.hxf_contract_batch.argtypes = [P, P, I64, I, I, I, P, I64, P, I64, P, I64, I, I,
+                                     C.POINTER(C.c_uint64)]
+    L.hxf_apply_tensor_3d.argtypes = [P, I, I, P, P, I, I, I, P, I64, P, I64, I]
+    L.hxf_flops_estimate.restype = C.c_uint64
+    L.hxf_flops_estimate.argtypes = [I, I, I, I]
     _lib = L
     return L
 
@@ -137,6 +153,27 @@ def check(rc: int) -> None:
 
 def launch_count() -> int:
     return int(lib().hxf_launch_count())
+
+
+def set_grid_cap(cap: int) -> int:
+    """Cap the operator / PCG vector kernel grids (test knob; 0 = none).  Returns the old cap."""
+    return int(lib().hxf_debug_set_grid_cap(int(cap)))
+
+
+def flops_estimate(p: int, q: int, m: int, mode: str) -> int:
+    """flops_estimate (contraction.cpp:334-340); mode 'interp' | 'grad'."""
+    return int(lib().hxf_flops_estimate(p, q, m, 1 if mode == "grad" else 0))
+
+
+def _empty_like_space(ref, n):
+    if isinstance(ref, np.ndarray):
+        return np.zeros(n)
+    import torch
+    return torch.empty(n, dtype=torch.float64, device=ref.device)
+
+
+def _len(a) -> int:
+    return 0 if a is None else int(a.size if isinstance(a, np.ndarray) else a.numel())
 
 
 def _ptr(a):
@@ -242,6 +279,96 @@ class Context:
                                       num_elements, n_L, cp,
                                       None if idx is None else idx.ctypes.data, dims_arr,
                                       0 if kind == "mass" else 1, op_, space))
+        return out
+
+
+    def contract_batch(self, matrix, n_out, n_in, dim, in_shape, ne, u, out=None,
+                       accumulate=False, flops=None):
+        """contract_batch (contraction.cpp:177-206).  `flops`: a one-element list
+        used as the FlopCounter (incremented by 2 per multiply-add)."""
+        M = np.ascontiguousarray(matrix, dtype=np.float64).reshape(-1)
+        u = _f64(u)
+        up, space = _ptr(u)
+        in_elem = int(in_shape[0]) * int(in_shape[1]) * int(in_shape[2])
+        out_n = ne * (in_elem // max(n_in, 1)) * n_out if n_in > 0 else 0
+        if out is None:
+            out = _empty_like_space(u, out_n)
+            if accumulate:
+                raise ValueError("contract_batch: accumulate needs an output array")
+        out = _f64(out)
+        shape = (C.c_int * 3)(*[int(v) for v in in_shape])
+        cnt = C.c_uint64(0 if flops is None else int(flops[0]))
+        check(lib().hxf_contract_batch(self._h, M.ctypes.data, M.size, n_out, n_in, dim, shape, ne,
+                                       up, _len(u), _ptr(out)[0], _len(out), int(bool(accumulate)),
+                                       space, C.byref(cnt)))
+        if flops is not None:
+            flops[0] = cnt.value
+        return out
+
+    def apply_tensor_3d(self, p, q, interp1d, grad1d, mode, direction, m, u):
+        """apply_tensor_3d (tensor_basis.cpp:73-99): one element, m components."""
+        B = np.ascontiguousarray(interp1d, dtype=np.float64)
+        G = np.ascontiguousarray(grad1d, dtype=np.float64)
+        grad, tr = mode == "grad", direction == "transpose"
+        nd3, nq3 = (p + 1) ** 3, q ** 3
+        out_e = nd3 if tr else (3 * nq3 if grad else nq3)
+        u = _f64(u)
+        up, space = _ptr(u)
+        out = _empty_like_space(u, m * out_e)
+        check(lib().hxf_apply_tensor_3d(self._h, p, q, B.ctypes.data, G.ctypes.data, int(grad),
+                                        int(tr), m, up, _len(u), _ptr(out)[0], _len(out), space))
+        return out
+
+
+class ElemRestriction:
+    """hxf_elem_restriction_* — the reference's ElemRestriction (restriction.hpp:14-50)."""
+
+    def __init__(self, ctx: Context, *, p, m, num_elements, n_L, indices=None, dims=None):
+        self.ctx = ctx
+        idx = None if indices is None else np.ascontiguousarray(indices, dtype=np.int64)
+        dims_arr = (C.c_int * 3)(*(dims if dims is not None else (0, 0, 0)))
+        self._h = C.c_void_p()
+        check(lib().hxf_elem_restriction_create(ctx.handle, p, m, num_elements, n_L,
+                                                None if idx is None else idx.ctypes.data,
+                                                dims_arr, C.byref(self._h)))
+        self.p, self.m, self.num_elements, self.n_L = p, m, num_elements, n_L
+        self.elem_size = (p + 1) ** 3
+
+    @property
+    def structured(self) -> bool:
+        return bool(lib().hxf_elem_restriction_is_structured(self._h))
+
+    def close(self):
+        if self._h:
+            lib().hxf_elem_restriction_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run(self, fn, v, n_out, *extra):
+        v = _f64(v)
+        vp, space = _ptr(v)
+        out = _empty_like_space(v, n_out)
+        check(fn(self._h, *extra, vp, _len(v), _ptr(out)[0], _len(out), space))
+        return out
+
+    def apply_g(self, l_vec):
+        return self._run(lib().hxf_elem_restriction_apply, l_vec,
+                         self.m * self.num_elements * self.elem_size, 0)
+
+    def apply_g_transpose(self, e_vec):
+        return self._run(lib().hxf_elem_restriction_apply, e_vec, self.m * self.n_L, 1)
+
+    def gather_scalar(self, e_scalar):
+        return self._run(lib().hxf_elem_restriction_gather_scalar, e_scalar, self.n_L)
+
+    def multiplicity(self):
+        out = np.zeros(self.n_L)
+        check(lib().hxf_elem_restriction_multiplicity(self._h, out.ctypes.data, out.size, HXF_HOST))
         return out
 
 

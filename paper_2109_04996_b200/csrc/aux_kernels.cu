@@ -88,6 +88,39 @@ __global__ void basis_apply_kernel(BasisDev bs, int nn, int nq, int mode, int di
   }
 }
 
+// contract_batch (contraction.cpp:177-206 -> contract_sf, :14-76): one output
+// entry per thread, grid-stride over the whole batch; contracted index
+// innermost and increasing, products and sums rounded separately, so each
+// entry is the reference's value bit for bit (accumulate: out += acc).
+__global__ void contract_batch_kernel(const double* __restrict__ M, int n_out, int n_in, int dim,
+                                      int s0, int s1, int s2, int64_t ne,
+                                      const double* __restrict__ in, double* __restrict__ out,
+                                      int accumulate) {
+  const int o0 = dim == 0 ? n_out : s0, o1 = dim == 1 ? n_out : s1;
+  const int o2 = dim == 2 ? n_out : s2;
+  const int64_t oe = (int64_t)o0 * o1 * o2, ie = (int64_t)s0 * s1 * s2;
+  const int64_t total = ne * oe;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / oe, r = t - e * oe;
+    const int a = (int)(r % o0), b = (int)((r / o0) % o1), c = (int)(r / ((int64_t)o0 * o1));
+    const double* ein = in + e * ie;
+    double acc = 0.0;
+    if (dim == 0) {
+      const double* col = ein + (int64_t)n_in * (b + (int64_t)s1 * c);
+      for (int k = 0; k < n_in; ++k) acc = dadd(acc, dmul(M[(int64_t)a * n_in + k], col[k]));
+    } else if (dim == 1) {
+      for (int k = 0; k < n_in; ++k)
+        acc = dadd(acc, dmul(M[(int64_t)b * n_in + k], ein[a + (int64_t)s0 * (k + (int64_t)s1 * c)]));
+    } else {
+      const int64_t plane = (int64_t)s0 * s1;
+      for (int k = 0; k < n_in; ++k)
+        acc = dadd(acc, dmul(M[(int64_t)c * n_in + k], ein[a + (int64_t)s0 * b + plane * k]));
+    }
+    out[t] = accumulate ? dadd(out[t], acc) : acc;
+  }
+}
+
 // apply_qf_mass / apply_qf_diffusion (qfunction.cpp:124-162)
 __global__ void qf_kernel(int kind, const double* __restrict__ qd, int nq, int64_t e0, int64_t ne,
                           const double* __restrict__ u, double* __restrict__ v) {
@@ -321,6 +354,18 @@ cudaError_t launch_basis_apply(cudaStream_t s, int p, int q, const double* B, co
   if (ne == 0) return cudaSuccess;
   basis_apply_kernel<<<(unsigned)ne, 128, smem, s>>>(BasisDev{B, G, Bt, Gt}, nn, q, mode, dir, ne,
                                                      in, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_contract_batch(cudaStream_t s, const double* M, int n_out, int n_in, int dim,
+                                  const int shape[3], int64_t ne, const double* in, double* out,
+                                  bool accumulate) {
+  const int64_t oe = (int64_t)shape[0] * shape[1] * shape[2] / n_in * n_out;
+  if (ne * oe == 0) return cudaSuccess;
+  contract_batch_kernel<<<grid_for(ne * oe, 256), 256, 0, s>>>(M, n_out, n_in, dim, shape[0],
+                                                               shape[1], shape[2], ne, in, out,
+                                                               accumulate ? 1 : 0);
   count_launch();
   return cudaGetLastError();
 }

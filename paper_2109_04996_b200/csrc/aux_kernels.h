@@ -15,6 +15,10 @@ struct Lattice {
 cudaError_t launch_basis_apply(cudaStream_t s, int p, int q, const double* B, const double* G,
                                const double* Bt, const double* Gt, int mode, int dir, int64_t ne,
                                const double* in, double* out);
+// contract_batch: one 1-D contraction of ne element blocks (device M, n_out x n_in)
+cudaError_t launch_contract_batch(cudaStream_t s, const double* M, int n_out, int n_in, int dim,
+                                  const int shape[3], int64_t ne, const double* in, double* out,
+                                  bool accumulate);
 cudaError_t launch_qfunction(cudaStream_t s, int kind, const double* qd, int nq, int64_t e0,
                              int64_t ne, const double* u, double* v);
 cudaError_t launch_restriction(cudaStream_t s, const Lattice& L, const int* idx, bool colorable,

@@ -24,29 +24,6 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 int g_sms = 0;
 
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return HXF_OK;
-  } catch (const HxfError& e) {
-    g_err = e.msg;
-    return e.code;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return HXF_ECUDA;
-  }
-}
-
-
-
-void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpy H2D");
-}
-void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpy D2H");
-}
-
 // Lagrange derivative matrix on the q quadrature points (barycentric form,
 // evaluated in long double): D[i][j] = l_j'(x_i).  Used for the collocated-
 // gradient factorisation of interpolating bases (op_kernel.cuh).
@@ -179,6 +156,14 @@ int dmma_warps() {
 
 int max_op_grid() { return num_sms() * 32; }
 
+namespace {
+std::atomic<int> g_grid_cap{[] {
+  const char* v = std::getenv("HXF_MAX_GRID");
+  return v ? std::max(0, std::atoi(v)) : 0;
+}()};
+}  // namespace
+int grid_cap() { return g_grid_cap.load(std::memory_order_relaxed); }
+
 bool centro_symmetric(int P, int Q, bool interp, const double* B, const double* D) {
   auto close = [](double a, double b, double scale) { return std::fabs(a - b) <= 1e-13 * scale; };
   double sb = 0, sd = 0;
@@ -215,6 +200,49 @@ void set_last_error(const char* msg) { g_err = msg; }
 }  // namespace hxf
 
 
+
+namespace hxf_detail {
+
+bool detect_box(int p, int64_t E, int64_t n_L, const int64_t* idx, const int dims[3],
+                const char* who, BoxDims* out) {
+  const int n1 = p + 1;
+  const int64_t S = int64_t(n1) * n1 * n1;
+  int64_t nx = dims ? dims[0] : 0, ny = dims ? dims[1] : 0, nz = dims ? dims[2] : 0;
+  if (!idx) {  // implicit structured box (dims validated here)
+    const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
+    if (nx < 1 || ny < 1 || nz < 1 || nx * ny * nz != E || NX * NY * NZ != n_L)
+      fail(HXF_EINVAL, std::string(who) + ": dims do not match num_elements / n_L");
+    *out = BoxDims{int(nx), int(ny), int(nz), NX, NY, NZ};
+    return true;
+  }
+  if (nx <= 0 || ny <= 0 || nz <= 0) {
+    const int64_t NXg = idx[n1];           // node of slot (0,1,0) in element 0
+    const int64_t NXNY = idx[n1 * n1];     // node of slot (0,0,1)
+    if (NXg <= 1 || (NXg - 1) % p || NXNY % NXg) return false;
+    nx = (NXg - 1) / p;
+    const int64_t NYg = NXNY / NXg;
+    if ((NYg - 1) % p) return false;
+    ny = (NYg - 1) / p;
+    if (nx * ny == 0 || E % (nx * ny)) return false;
+    nz = E / (nx * ny);
+  }
+  if (nx * ny * nz != E) return false;
+  const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
+  if (NX * NY * NZ != n_L) return false;
+  for (int64_t e = 0; e < E; ++e) {
+    const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
+    const int64_t* row = idx + e * S;
+    int64_t s = 0;
+    for (int kz = 0; kz <= p; ++kz)
+      for (int ky = 0; ky <= p; ++ky)
+        for (int kx = 0; kx <= p; ++kx, ++s)
+          if (row[s] != (ex * p + kx) + NX * ((ey * p + ky) + NY * (ez * p + kz))) return false;
+  }
+  *out = BoxDims{int(nx), int(ny), int(nz), NX, NY, NZ};
+  return true;
+}
+
+}  // namespace hxf_detail
 
 namespace {
 
@@ -316,52 +344,18 @@ std::vector<int64_t> sorted_unique(const int64_t* v, int64_t n) {
 }
 
 // Recognise the reference's structured-box numbering (mesh.cpp:80-104) and
-// verify it entry by entry (bit-exact assembly map).
+// verify it entry by entry (bit-exact assembly map).  idx == nullptr: the
+// implicit box given by dims (checked against E and n_L; `who` names the
+// caller in the error message).
 bool detect_structured(hxf_op* op, const int64_t* idx, const int dims[3]) {
-  const int p = op->p, n1 = p + 1;
-  const int64_t S = int64_t(n1) * n1 * n1;
-  int64_t nx = dims ? dims[0] : 0, ny = dims ? dims[1] : 0, nz = dims ? dims[2] : 0;
-  if (!idx) {  // implicit structured box (dims validated by the caller)
-    const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
-    if (nx * ny * nz != op->E || NX * NY * NZ != op->n_L)
-      fail(HXF_EINVAL, "make_operator: dims do not match num_elements / n_L");
-    op->nx = int(nx);
-    op->ny = int(ny);
-    op->nz = int(nz);
-    op->NX = NX;
-    op->NY = NY;
-    op->NZ = NZ;
-    return true;
-  }
-  if (nx <= 0 || ny <= 0 || nz <= 0) {
-    const int64_t NXg = idx[n1];           // node of slot (0,1,0) in element 0
-    const int64_t NXNY = idx[n1 * n1];     // node of slot (0,0,1)
-    if (NXg <= 1 || (NXg - 1) % p || NXNY % NXg) return false;
-    nx = (NXg - 1) / p;
-    const int64_t NYg = NXNY / NXg;
-    if ((NYg - 1) % p) return false;
-    ny = (NYg - 1) / p;
-    if (nx * ny == 0 || op->E % (nx * ny)) return false;
-    nz = op->E / (nx * ny);
-  }
-  if (nx * ny * nz != op->E) return false;
-  const int64_t NX = nx * p + 1, NY = ny * p + 1, NZ = nz * p + 1;
-  if (NX * NY * NZ != op->n_L) return false;
-  for (int64_t e = 0; e < op->E; ++e) {
-    const int64_t ex = e % nx, ey = (e / nx) % ny, ez = e / (nx * ny);
-    const int64_t* row = idx + e * S;
-    int64_t s = 0;
-    for (int kz = 0; kz <= p; ++kz)
-      for (int ky = 0; ky <= p; ++ky)
-        for (int kx = 0; kx <= p; ++kx, ++s)
-          if (row[s] != (ex * p + kx) + NX * ((ey * p + ky) + NY * (ez * p + kz))) return false;
-  }
-  op->nx = int(nx);
-  op->ny = int(ny);
-  op->nz = int(nz);
-  op->NX = NX;
-  op->NY = NY;
-  op->NZ = NZ;
+  BoxDims b;
+  if (!detect_box(op->p, op->E, op->n_L, idx, dims, "make_operator", &b)) return false;
+  op->nx = b.nx;
+  op->ny = b.ny;
+  op->nz = b.nz;
+  op->NX = b.NX;
+  op->NY = b.NY;
+  op->NZ = b.NZ;
   return true;
 }
 
@@ -411,12 +405,21 @@ void pcg_prepare(hxf_op* op, int limit) {
     op->ev.push_back(e);
   }
   const size_t n = size_t(op->size());
+  // every work buffer a cached solve graph captured by address: growing one
+  // (e.g. w_hist for a longer tolerance solve) frees the old allocation, so
+  // the graphs holding it are dropped (they would replay into freed memory)
+  auto captured = [op] {
+    return std::vector<const void*>{op->w_r.p, op->w_p.p, op->w_p2.p, op->w_Ap.p,
+                                    op->w_vpart.p, op->w_hist.p, op->w_halo.p};
+  };
+  const std::vector<const void*> before = captured();
   op->w_r.ensure(n);
   op->w_p.ensure(n);
   if (xbatch()) op->w_p2.ensure(n);
   op->w_Ap.ensure(n);
   op->w_vpart.ensure(size_t(3 * vec_grid()));  // per-CTA partials (<= 3 per CTA)
   op->w_hist.ensure(size_t(limit) + 2);
+  if (captured() != before) op->drop_graphs();
 }
 
 // the solve's kernels (captured into a graph or run eagerly)
@@ -577,6 +580,12 @@ extern "C" {
 const char* hxf_last_error(void) { return g_err.c_str(); }
 int hxf_abi_version(void) { return HXF_ABI_VERSION; }
 int64_t hxf_launch_count(void) { return g_launches.load(); }
+
+int hxf_debug_set_grid_cap(int cap) {
+  const int old = g_grid_cap.load();
+  g_grid_cap.store(cap > 0 ? cap : 0);
+  return old;
+}
 
 int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out) {
   return guarded([&] {

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -34,6 +35,13 @@ T* dalloc(size_t n) {
   void* p = nullptr;
   ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
   return static_cast<T*>(p);
+}
+
+inline void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpy H2D");
+}
+inline void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpy D2H");
 }
 
 struct DevVec {
@@ -169,3 +177,31 @@ bool overlap_enabled();  // HXF_OVERLAP=0: exchange after the whole apply
 void set_last_error(const char* msg);  // capi.cu: the thread's hxf_last_error()
 void op_set_constrained(hxf_op* op, double* v, double value, cudaStream_t s);
 }  // namespace hxf
+
+namespace hxf_detail {
+// Run f, mapping HxfError / std::exception onto the C status codes (message
+// left in the thread's hxf_last_error()).
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HXF_OK;
+  } catch (const HxfError& e) {
+    hxf::set_last_error(e.msg.c_str());
+    return e.code;
+  } catch (const std::exception& e) {
+    hxf::set_last_error(e.what());
+    return HXF_ECUDA;
+  }
+}
+
+// Structured-box lattice of a restriction (capi.cu): the reference's
+// numbering (mesh.cpp:80-104) recognised and verified entry by entry, or the
+// implicit box given by dims when idx is NULL.
+struct BoxDims {
+  int nx = 0, ny = 0, nz = 0;
+  int64_t NX = 0, NY = 0, NZ = 0;
+};
+bool detect_box(int p, int64_t E, int64_t n_L, const int64_t* idx, const int dims[3],
+                const char* who, BoxDims* out);
+}  // namespace hxf_detail

@@ -77,6 +77,17 @@ cudaError_t launch_op(int P, int Q, int NC, bool interp, int qk, const OpParams&
 // Upper bound on the grid of any launch_op() call (partials buffer size).
 int max_op_grid();
 
+// Test knob (hxf_debug_set_grid_cap / HXF_MAX_GRID): caps the grid of the
+// operator and PCG vector kernels so small meshes run the multi-element-per-
+// CTA (grid-stride) paths the full-size configurations take.  0 = no cap.
+int grid_cap();
+inline int capped_grid(int64_t want, int max_ctas) {
+  int64_t g = want < max_ctas ? want : max_ctas;
+  const int cap = grid_cap();
+  if (cap > 0 && g > cap) g = cap;
+  return (int)g;
+}
+
 // The even-odd line / pencil kernels need centro-symmetric 1-D matrices
 // (B[q-1-i][p-j] = B[i][j], D[q-1-i][q-1-j] = -D[i][j]); otherwise the general
 // kernel runs.

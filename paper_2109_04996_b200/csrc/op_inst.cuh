@@ -40,7 +40,7 @@ cudaError_t run(const OpParams& prm, const double* B, const double* D, cudaStrea
   if (T::INTERP) std::memcpy(mats.B, B, sizeof(double) * T::Q * T::P);
   std::memcpy(mats.D, D, sizeof(double) * T::Q * T::Q);
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
-  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  const int grid = capped_grid(nsteps, max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
   kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
@@ -73,7 +73,7 @@ cudaError_t run_line(const OpParams& prm, const double* B, const double* D, cuda
   if (T::INTERP) std::memcpy(mats.B, B, sizeof(double) * T::Q * T::P);
   std::memcpy(mats.D, D, sizeof(double) * T::Q * T::Q);
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
-  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  const int grid = capped_grid(nsteps, max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
   kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm, mats);
@@ -102,7 +102,7 @@ cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int
   if (prm.elist) return cudaErrorNotSupported;  // no element-list support
   if (!prm.D) return cudaErrorInvalidValue;
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
-  const int grid = (int)(nsteps < max_ctas ? nsteps : max_ctas);
+  const int grid = capped_grid(nsteps, max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
   kern<<<grid, T::NT, T::SMEM_BYTES, s>>>(prm);
@@ -126,7 +126,7 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
     max_ctas = nb * num_sms();
   }
   if (!prm.D) return cudaErrorInvalidValue;
-  const int grid = (int)(prm.E < max_ctas ? prm.E : max_ctas);
+  const int grid = capped_grid(prm.E, max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
   const cudaError_t err = launch_pdl_if(pdl_enabled() || prm.pdl, kern, dim3(grid), dim3(T::NT),

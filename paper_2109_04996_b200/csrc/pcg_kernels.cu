@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(VT)
 }
 
 // ------------------------------------------------------------------ host side
-int vec_grid() { return num_sms() * 4; }
+int vec_grid() { return capped_grid(int64_t(num_sms()) * 4, num_sms() * 4); }
 
 namespace {
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -73,3 +73,21 @@ def test_host_tables_match_oracle_bitwise():
             b = hx.basis(p, kind, q)
             assert np.array_equal(b.interp1d, t[f"basis_{kind}_{p}_B"])
             assert np.array_equal(b.grad1d, t[f"basis_{kind}_{p}_G"])
+
+
+def test_flops_estimate_matches_reference_formula():
+    """hxf_flops_estimate is host arithmetic (no device): the reference's
+    known answers (test_contraction.cpp:122-129) and the oracle's closed form."""
+    import oracle
+
+    assert capi.flops_estimate(1, 1, 1, "interp") == 28
+    assert capi.flops_estimate(1, 1, 1, "grad") == 84
+    for p in range(1, 16):
+        for q in (p + 1, p + 2):
+            for m in (1, 3):
+                for mode in ("interp", "grad"):
+                    assert capi.flops_estimate(p, q, m, mode) == oracle.flops_estimate(p, q, m, mode)
+    # per-apply counts recorded by the reference's acceptance run
+    # (acceptance.cpp:393-404, test_output.txt:21): 8 elements x (B + B^T)
+    assert 8 * 2 * capi.flops_estimate(3, 4, 1, "grad") == 73728   # BP5 p=3 2^3
+    assert 8 * 2 * capi.flops_estimate(3, 5, 1, "grad") == 117120  # BP3 p=3 2^3

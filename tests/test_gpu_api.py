@@ -154,3 +154,27 @@ def test_pcg_host_batch_matches_single_solves():
             k = min(len(rep["residual_history"]), len(rep1["residual_history"]))
             assert oracle.rel_max_diff(rep1["residual_history"][:k],
                                        rep["residual_history"][:k]) <= 1e-10
+
+
+def test_cached_solve_graph_survives_buffer_growth():
+    """A fixed-iteration solve is captured into a CUDA graph; a following
+    tolerance solve with a larger iteration limit regrows the history buffer
+    (and frees the old one).  Replaying the first solve must not write into
+    the freed buffer: same residual history and iterate as the first time."""
+    prob = hx.setup("bp5", degree=3, dims=(3, 3, 3), deform="sine")
+    x1, r1 = prob.solve(tol=1e-8, fixed_iterations=20)
+    x2, r2 = prob.solve(tol=1e-12, max_iter=2000)
+    assert r2["converged"] and r2["iterations"] > 20
+    x3, r3 = prob.solve(tol=1e-8, fixed_iterations=20)
+    assert np.array_equal(r1["residual_history"], r3["residual_history"])
+    assert np.array_equal(x1, x3)
+    # and the device-pointer entry point, same operator, alternating limits
+    import torch
+    b = torch.from_numpy(prob.rhs).cuda()
+    xs = [torch.zeros(prob.size, dtype=torch.float64, device="cuda") for _ in range(3)]
+    ra = prob.pcg_device(b.data_ptr(), xs[0].data_ptr(), fixed_iterations=20)
+    prob.pcg_device(b.data_ptr(), xs[1].data_ptr(), fixed_iterations=50)
+    rc = prob.pcg_device(b.data_ptr(), xs[2].data_ptr(), fixed_iterations=20)
+    torch.cuda.synchronize()
+    assert np.array_equal(ra["residual_history"], rc["residual_history"])
+    assert torch.equal(xs[0], xs[2])

@@ -205,3 +205,65 @@ def test_device_memspace_and_fused_dot(ctx):
     yd = op.apply(xd, stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert oracle.rel_max_diff(y_ref, yd.cpu().numpy()) <= APPLY_TOL
+
+
+# ---- every K1 family's multi-element-per-CTA loop, oracle-checked ----------
+# The operator kernels are persistent (grid = min(E, occupancy x SMs)), so the
+# small meshes above give each CTA at most one element, while the full-size
+# configurations loop ~26 times per CTA (next-element gather pipeline, factor
+# refill + mbarrier phase flips, line-kernel step refills).  Capping the grid
+# runs those loops on meshes the oracle finishes in milliseconds.
+KERNEL_FAMILIES = [
+    ("bp5", 7, (5, 4, 3)),   # DMMA, one component
+    ("bp6", 7, (2, 3, 2)),   # DMMA, three components
+    ("bp6", 6, (3, 2, 2)),   # zero-padded DMMA tile
+    ("bp6", 5, (3, 3, 2)),   # pencil
+    ("bp6", 8, (2, 2, 3)),   # pencil
+    ("bp6", 2, (4, 3, 3)),   # pencil, small p
+    ("bp5", 4, (4, 3, 3)),   # line, collocated
+    ("bp5", 11, (2, 2, 2)),  # line, late z-derivative form
+    ("bp3", 7, (3, 3, 2)),   # line, interpolating (staged factors)
+    ("bp6", 4, (3, 2, 2)),   # line, three components
+    ("bp4", 3, (3, 2, 3)),   # line, interpolating, three components
+    ("bp1", 3, (5, 4, 3)),   # line, mass
+    ("bp2", 4, (3, 3, 2)),   # line, mass, three components
+    ("bp5", 1, (7, 6, 5)),   # line, 64-thread CTAs
+]
+
+
+@pytest.fixture
+def grid_cap():
+    old = capi.set_grid_cap(0)
+    yield capi.set_grid_cap
+    capi.set_grid_cap(old)
+
+
+@pytest.mark.parametrize("cap", [1, 3, 7])
+@pytest.mark.parametrize("bp,p,dims", KERNEL_FAMILIES)
+def test_apply_multi_element_per_cta(ctx, grid_cap, cap, bp, p, dims):
+    grid_cap(cap)
+    pr = oracle.setup(bp, p, dims, "sine")
+    op = op_from_oracle(ctx, pr)
+    x = oracle.seeded_uniform(pr.size, 99)
+    y = op.apply(x)
+    assert oracle.rel_max_diff(pr.apply(x), y) <= APPLY_TOL
+    cons = pr.constrained
+    for c in range(pr.components):
+        assert np.array_equal(y[c * pr.num_nodes + cons], x[c * pr.num_nodes + cons])
+
+
+@pytest.mark.parametrize("cap", [2, 5])
+@pytest.mark.parametrize("bp,p,dims", [("bp5", 7, (4, 4, 3)), ("bp6", 5, (3, 3, 2)),
+                                       ("bp3", 4, (3, 3, 3)), ("bp2", 3, (3, 2, 2))])
+def test_pcg_history_multi_element_per_cta(ctx, grid_cap, cap, bp, p, dims):
+    """20 fixed iterations (the bench step) with capped operator AND vector
+    grids: residual history and iterate against the oracle's."""
+    grid_cap(cap)
+    pr = oracle.setup(bp, p, dims, "sine")
+    op = op_from_oracle(ctx, pr)
+    d = pr.diagonal()
+    x, rep = op.pcg(pr.rhs, d, tol=1e-8, fixed_iterations=20)
+    xr, rrep = pr.solve(tol=1e-8, fixed_iterations=20)
+    assert rep["iterations"] == rrep["iterations"] == 20
+    assert oracle.rel_max_diff(rrep["residual_history"], rep["residual_history"]) <= 1e-10
+    assert oracle.rel_max_diff(xr, x) <= 1e-10
