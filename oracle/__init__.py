@@ -369,6 +369,16 @@ class RefWithBackend:
         L.orh_apply.argtypes = [P, I, pd, pd]
         L.orh_diagonal.argtypes = [P, I, pd]
         L.orh_solve.argtypes = [P, I, D, I, pd, pi, pi]
+        U64p = C.POINTER(C.c_uint64)
+        I64 = C.c_int64
+        L.orh_scale_qdata.argtypes = [P, D]
+        L.orh_apply_counted.argtypes = [P, I, pd, pd, U64p]
+        L.orh_restriction.argtypes = [P, I, I, pd, I64, pd, I64]
+        L.orh_basis.argtypes = [P, I, I, I, I, I64, pd, I64, pd, I64, U64p]
+        L.orh_contract.argtypes = [I, pd, I64, I, I, I, C.POINTER(C.c_int), I64, pd, I64, pd, I64,
+                                   I, U64p]
+        L.orh_flops_estimate.restype = C.c_uint64
+        L.orh_flops_estimate.argtypes = [I, I, I, I, I]
         self._L = L
         dims = tuple(int(d) for d in dims)
         h = L.orh_setup(BP_IDS[bp], degree, dims[0], dims[1], dims[2],
@@ -392,6 +402,48 @@ class RefWithBackend:
         d = np.zeros(self.size)
         self._ck(self._L.orh_diagonal(self._h, which, _dp(d)))
         return d
+
+    def scale_qdata(self, s: float) -> None:
+        """Scale the reference operator's qdata in place (same addresses)."""
+        self._L.orh_scale_qdata(self._h, float(s))
+
+    def apply_counted(self, x, which):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.size)
+        cnt = C.c_uint64(0)
+        self._ck(self._L.orh_apply_counted(self._h, which, _dp(x), _dp(y), C.byref(cnt)))
+        return y, int(cnt.value)
+
+    def restriction(self, which, what, v, n_out):
+        """what: 'apply_g' | 'apply_g_transpose' | 'gather_scalar' | 'multiplicity'."""
+        code = ["apply_g", "apply_g_transpose", "gather_scalar", "multiplicity"].index(what)
+        v = np.ascontiguousarray(v if v is not None else np.zeros(0), dtype=np.float64)
+        out = np.zeros(n_out)
+        self._ck(self._L.orh_restriction(self._h, which, code, _dp(v), v.size, _dp(out), out.size))
+        return out
+
+    def basis(self, which, what, mode, direction, ne_or_m, v, n_out):
+        """what: 'batch' (apply_basis_batch, ne blocks) | 'tensor3d' (m components)."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros(n_out)
+        cnt = C.c_uint64(0)
+        self._ck(self._L.orh_basis(self._h, which, 0 if what == "batch" else 1,
+                                   int(mode == "grad"), int(direction == "transpose"), ne_or_m,
+                                   _dp(v), v.size, _dp(out), out.size, C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def contract(self, which, M, n_out, n_in, dim, shape, ne, u, out, accumulate):
+        M = np.ascontiguousarray(M, dtype=np.float64)
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.array(out, dtype=np.float64, copy=True)
+        sh = (C.c_int * 3)(*shape)
+        cnt = C.c_uint64(0)
+        self._ck(self._L.orh_contract(which, _dp(M), M.size, n_out, n_in, dim, sh, ne, _dp(u),
+                                      u.size, _dp(out), out.size, int(accumulate), C.byref(cnt)))
+        return out, int(cnt.value)
+
+    def flops_estimate(self, which, p, q, m, mode):
+        return int(self._L.orh_flops_estimate(which, p, q, m, int(mode == "grad")))
 
     def solve(self, which, tol=1e-8, jacobi=True):
         x = np.zeros(self.size)

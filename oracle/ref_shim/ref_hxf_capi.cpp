@@ -6,6 +6,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <span>
 #include <string>
 
 #include "hexfem/bench.hpp"
@@ -93,5 +94,106 @@ int orh_solve(void* hv, int which, double tol, int jacobi, double* x, int* iters
 }
 
 void orh_release() { hxf_backend::release_all(); }
+
+// Scale the operator's stored qdata in place (same addresses, new contents):
+// the backend must notice and re-upload (its side table is content-checked).
+void orh_scale_qdata(void* hv, double s) {
+  auto& op = static_cast<H*>(hv)->prob.op;
+  for (auto* qd : {&op.mass_qdata, &op.diff_qdata})
+    if (qd->has_value())
+      for (double& v : (*qd)->values) v *= s;
+}
+
+// operator_apply with a FlopCounter attached: which = 0 the reference's
+// instrumented count, 1 the backend's credited count.
+int orh_apply_counted(void* hv, int which, const double* x, double* y, uint64_t* flops) {
+  auto* h = static_cast<H*>(hv);
+  const size_t n = size_t(h->prob.op.size());
+  return guarded([&] {
+    FlopCounter fc;
+    MatFreeOperator op = h->prob.op;  // a copy: same arrays (shared qdata), new address
+    op.plan.flops = &fc;
+    if (which == 0)
+      operator_apply(op, {x, n}, {y, n}, h->pool.get());
+    else
+      hxf_backend::operator_apply(op, {x, n}, {y, n});
+    *flops = fc.count();
+  });
+}
+
+// Restriction surface on the problem's own ElemRestriction: what = 0 apply_g,
+// 1 apply_g_transpose, 2 gather_scalar, 3 multiplicity.
+int orh_restriction(void* hv, int which, int what, const double* in, int64_t n_in, double* out,
+                    int64_t n_out) {
+  auto* h = static_cast<H*>(hv);
+  const auto& r = h->prob.op.restriction;
+  return guarded([&] {
+    std::span<const double> a(in, size_t(n_in));
+    std::span<double> b(out, size_t(n_out));
+    if (what == 0) which ? hxf_backend::apply_g(r, a, b) : apply_g(r, a, b, h->pool.get());
+    if (what == 1)
+      which ? hxf_backend::apply_g_transpose(r, a, b) : apply_g_transpose(r, a, b, h->pool.get());
+    if (what == 2)
+      which ? hxf_backend::gather_scalar(r, a, b) : gather_scalar(r, a, b, h->pool.get());
+    if (what == 3) {
+      auto m = which ? hxf_backend::multiplicity(r) : multiplicity(r);
+      std::memcpy(out, m.data(), m.size() * sizeof(double));
+    }
+  });
+}
+
+// Basis surface on the problem's own TensorBasis: what = 0 apply_basis_batch
+// (ne blocks), 1 apply_tensor_3d (m components); counted flops out.
+int orh_basis(void* hv, int which, int what, int grad, int transpose, int64_t ne_or_m,
+              const double* in, int64_t n_in, double* out, int64_t n_out, uint64_t* flops) {
+  auto* h = static_cast<H*>(hv);
+  const auto& basis = h->prob.basis;
+  return guarded([&] {
+    const EvalMode mode = grad ? EvalMode::Grad : EvalMode::Interp;
+    const EvalDirection dir = transpose ? EvalDirection::Transpose : EvalDirection::Forward;
+    std::span<const double> a(in, size_t(n_in));
+    std::span<double> b(out, size_t(n_out));
+    FlopCounter fc;
+    KernelPlan plan;
+    plan.p = basis.p;
+    plan.q = basis.q;
+    plan.flops = &fc;
+    ContractionScratch scratch;
+    if (what == 0)
+      which ? hxf_backend::apply_basis_batch(plan, basis, mode, dir, ne_or_m, a, b, scratch)
+            : apply_basis_batch(plan, basis, mode, dir, ne_or_m, a, b, scratch);
+    else
+      which ? hxf_backend::apply_tensor_3d(basis, mode, dir, int(ne_or_m), a, b)
+            : apply_tensor_3d(basis, mode, dir, int(ne_or_m), a, b);
+    *flops = fc.count();
+  });
+}
+
+int orh_contract(int which, const double* M, int64_t m_len, int n_out, int n_in, int dim,
+                 const int* shape, int64_t ne, const double* in, int64_t n_in_len, double* out,
+                 int64_t n_out_len, int accumulate, uint64_t* flops) {
+  return guarded([&] {
+    FlopCounter fc;
+    KernelPlan plan;
+    plan.flops = &fc;
+    std::span<const double> mm(M, size_t(m_len)), a(in, size_t(n_in_len));
+    std::span<double> b(out, size_t(n_out_len));
+    const std::array<int, 3> sh{shape[0], shape[1], shape[2]};
+    if (which)
+      hxf_backend::contract_batch(plan, mm, n_out, n_in, dim, sh, ne, a, b, accumulate != 0);
+    else
+      contract_batch(plan, mm, n_out, n_in, dim, sh, ne, a, b, accumulate != 0);
+    *flops = fc.count();
+  });
+}
+
+uint64_t orh_flops_estimate(int which, int p, int q, int m, int grad) {
+  KernelPlan plan;
+  plan.p = p;
+  plan.q = q;
+  plan.m = m;
+  const EvalMode mode = grad ? EvalMode::Grad : EvalMode::Interp;
+  return which ? hxf_backend::flops_estimate(plan, mode) : flops_estimate(plan, mode);
+}
 
 }  // extern "C"

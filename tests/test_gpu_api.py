@@ -158,23 +158,28 @@ def test_pcg_host_batch_matches_single_solves():
 
 def test_cached_solve_graph_survives_buffer_growth():
     """A fixed-iteration solve is captured into a CUDA graph; a following
-    tolerance solve with a larger iteration limit regrows the history buffer
-    (and frees the old one).  Replaying the first solve must not write into
-    the freed buffer: same residual history and iterate as the first time."""
-    prob = hx.setup("bp5", degree=3, dims=(3, 3, 3), deform="sine")
-    x1, r1 = prob.solve(tol=1e-8, fixed_iterations=20)
-    x2, r2 = prob.solve(tol=1e-12, max_iter=2000)
-    assert r2["converged"] and r2["iterations"] > 20
-    x3, r3 = prob.solve(tol=1e-8, fixed_iterations=20)
-    assert np.array_equal(r1["residual_history"], r3["residual_history"])
-    assert np.array_equal(x1, x3)
-    # and the device-pointer entry point, same operator, alternating limits
+    tolerance solve (another right-hand side) with a larger iteration limit
+    regrows the history buffer and frees the old one.  Replaying the first
+    solve must report ITS history, not whatever the regrown buffer holds (a
+    stale graph would write into the freed allocation).  Runs differ only by
+    the RED scatter's rounding order, hence the 1e-12 bar."""
     import torch
+
+    prob = hx.setup("bp5", degree=3, dims=(3, 3, 3), deform="sine")
+    n = prob.size
     b = torch.from_numpy(prob.rhs).cuda()
-    xs = [torch.zeros(prob.size, dtype=torch.float64, device="cuda") for _ in range(3)]
-    ra = prob.pcg_device(b.data_ptr(), xs[0].data_ptr(), fixed_iterations=20)
-    prob.pcg_device(b.data_ptr(), xs[1].data_ptr(), fixed_iterations=50)
-    rc = prob.pcg_device(b.data_ptr(), xs[2].data_ptr(), fixed_iterations=20)
+    b2 = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, n)).cuda()
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    ra = prob.pcg_device(b.data_ptr(), x.data_ptr(), fixed_iterations=20)
+    rb = prob.pcg_device(b2.data_ptr(), x.data_ptr(), tol=1e-12, max_iter=2000)
+    assert rb["converged"] and rb["iterations"] > 20
+    rc = prob.pcg_device(b.data_ptr(), x.data_ptr(), fixed_iterations=20)
     torch.cuda.synchronize()
-    assert np.array_equal(ra["residual_history"], rc["residual_history"])
-    assert torch.equal(xs[0], xs[2])
+    assert oracle.rel_max_diff(ra["residual_history"], rc["residual_history"]) <= 1e-12
+    assert oracle.rel_max_diff(rb["residual_history"][:21], rc["residual_history"]) > 1e-3
+    # the host-vector API on the same operator, alternating limits
+    x1, r1 = prob.solve(tol=1e-8, fixed_iterations=20)
+    prob.solve(tol=1e-12, max_iter=2000)
+    x3, r3 = prob.solve(tol=1e-8, fixed_iterations=20)
+    assert oracle.rel_max_diff(r1["residual_history"], r3["residual_history"]) <= 1e-12
+    assert oracle.rel_max_diff(x1, x3) <= 1e-12
