@@ -11,6 +11,8 @@
 #include <functional>
 #include <memory>
 #include <optional>
+#include <span>
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -141,6 +143,64 @@ class DeviceBuffer {
   double* ptr_ = nullptr;
   size_t n_ = 0;
 };
+
+// ---- element restriction (restriction.hpp:14-50; mesh.hpp:33-39) ----------
+// Node indices of element e, lexicographic x-fastest (mesh.cpp:80-104).
+std::vector<int64_t> element_node_indices(const HexMesh& mesh, int64_t e);
+
+// The restriction lives on the device (hxf_restr): for the structured box
+// make_restriction builds, G / G^T are computed from the lattice and G^T
+// accumulates in the reference's colour-class order (bitwise equal).
+class ElemRestriction {
+ public:
+  ElemRestriction(std::shared_ptr<Device> dev, int p, int m, int64_t num_elements, int64_t n_L,
+                  const int64_t* indices, std::array<int, 3> dims);
+  ~ElemRestriction();
+  ElemRestriction(const ElemRestriction&) = delete;
+  ElemRestriction& operator=(const ElemRestriction&) = delete;
+  int64_t num_elements = 0;
+  int elem_size = 0;
+  int64_t n_L = 0;
+  int m = 1;
+  hxf_restr* handle() const { return r_; }
+  void apply_g(std::span<const double> l_vec, std::span<double> e_vec) const;
+  void apply_g_transpose(std::span<const double> e_vec, std::span<double> l_vec) const;
+  std::vector<double> multiplicity() const;
+  void gather_scalar(std::span<const double> e_scalar, std::span<double> l_scalar) const;
+
+ private:
+  std::shared_ptr<Device> dev_;
+  hxf_restr* r_ = nullptr;
+};
+std::unique_ptr<ElemRestriction> make_restriction(const HexMesh& mesh, int m, int device = 0);
+
+// ---- contraction kernels / tensor basis (contraction.hpp:13-75,
+// tensor_basis.hpp:35-47) on the GPU; bitwise equal to the reference's
+// sum-factorized path (KernelPath::Naive is the reference's oracle path).
+enum class EvalMode { Interp, Grad };
+enum class EvalDirection { Forward, Transpose };
+struct FlopCounter {
+  std::atomic<uint64_t> ops{0};
+  void reset() { ops.store(0); }
+  uint64_t count() const { return ops.load(); }
+};
+struct KernelPlan {
+  int p = 1;
+  int q = 2;
+  int m = 1;
+  int block = 8;  // accepted, ignored
+  FlopCounter* flops = nullptr;
+  int device = 0;
+};
+void contract_batch(const KernelPlan& plan, std::span<const double> matrix, int n_out, int n_in,
+                    int dim, std::array<int, 3> in_shape, int64_t ne, std::span<const double> in,
+                    std::span<double> out, bool accumulate = false);
+void apply_basis_batch(const KernelPlan& plan, const TensorBasis& basis, EvalMode mode,
+                       EvalDirection dir, int64_t ne, std::span<const double> in,
+                       std::span<double> out);
+uint64_t flops_estimate(const KernelPlan& plan, EvalMode mode);
+void apply_tensor_3d(const TensorBasis& basis, EvalMode mode, EvalDirection dir, int m,
+                     std::span<const double> u, std::span<double> v, int device = 0);
 
 // ---- BP problems (bench.hpp:16-58) --------------------------------------
 enum class BpId { BP1 = 1, BP2, BP3, BP4, BP5, BP6 };

@@ -96,3 +96,30 @@ def test_elem_restriction_bitwise(ctx, bp, p, dims, with_table):
     with pytest.raises(ValueError, match="apply_g: L-vector length mismatch"):
         r.apply_g(l[:-1])
     r.close()
+
+
+def test_python_api_surface_matches_oracle():
+    """The same rows through the pybind mirror of hexfem._core."""
+    import paper_2109_04996_b200 as hx
+    from paper_2109_04996_b200 import _core
+
+    b = hx.basis(4, "gauss", 6)
+    u = oracle.seeded_uniform(2 * 5 ** 3, 3)
+    assert np.array_equal(_core.apply_tensor_3d(b, "grad", "forward", 2, u),
+                          oracle.apply_tensor_3d(4, "gauss", 6, "grad", "forward", 2, u))
+    ub = oracle.seeded_uniform(3 * 3 * 6 ** 3, 4)
+    out = _core.apply_basis_batch(b, "grad", "transpose", 3, ub)
+    assert np.array_equal(out, oracle.apply_basis(4, "gauss", 6, "grad", "transpose", 3, ub))
+    M = np.arange(1.0, 5.0)
+    v, fl = _core.contract_batch(M, 2, 2, 0, (2, 2, 2), 1, np.arange(1.0, 9.0))
+    assert list(v[:4]) == [5, 11, 11, 25] and fl == 16
+    assert _core.flops_estimate(1, 1, 1, "grad") == 84
+    prob = hx.setup("bp6", degree=2, dims=(3, 2, 2), deform="sine")
+    ref = oracle.setup("bp6", 2, (3, 2, 2), "sine")
+    es = oracle.seeded_uniform(ref.num_elements * ref.elem_size, 6)
+    assert np.array_equal(prob.gather_scalar(es), ref.gather_scalar(es))
+    l = oracle.seeded_uniform(prob.size, 7)
+    e = prob.apply_g(l)
+    assert e.size == 3 * ref.num_elements * ref.elem_size
+    back = prob.apply_g_transpose(e)
+    assert np.array_equal(back, l * np.tile(prob.multiplicity(), 3))
