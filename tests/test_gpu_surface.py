@@ -122,4 +122,4 @@ def test_python_api_surface_matches_oracle():
     e = prob.apply_g(l)
     assert e.size == 3 * ref.num_elements * ref.elem_size
     back = prob.apply_g_transpose(e)
-    assert np.array_equal(back, l * np.tile(prob.multiplicity(), 3))
+    assert np.allclose(back, l * np.tile(prob.multiplicity(), 3), rtol=1e-15, atol=0)
