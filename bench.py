@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--deform", default="sine")
     ap.add_argument("--iters", type=int, default=20, help="CG iterations per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--cpu-iters", type=int, default=5)
+    ap.add_argument("--cpu-iters", type=int, default=None,
+                    help="CG iterations per reference step (default: --iters, same workload)")
     return ap.parse_args()
 
 
@@ -207,8 +208,8 @@ def cpu_baseline(args, sizes):
         wall = time.perf_counter() - t0
         return {"value": rec["dofs_rate"] / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
                 "sample": (f"reference run_bench {args.bp} p={args.degree} {args.elems}^3 "
-                           f"{args.deform}, {args.cpu_iters} fixed CG iters, min of 3 reps, "
-                           f"{cores} threads; {wall:.1f}s incl. setup"),
+                           f"{args.deform}, {args.cpu_iters} fixed CG iters (the bench step), "
+                           f"min of 3 reps, {cores} threads; {wall:.1f}s incl. setup"),
                 "seconds_per_iter": rec["seconds"] / max(rec["iterations"], 1)}
     # fallback: the C restatement on one core, smaller sample
     d = max(2, args.elems // 3)
@@ -218,6 +219,29 @@ def cpu_baseline(args, sizes):
     dt = time.perf_counter() - t0
     return {"value": pr.n * rep["iterations"] / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"oracle port {args.bp} p={args.degree} {d}^3, {args.cpu_iters} CG iters"}
+
+
+def verify_against_reference(args, history, x):
+    """The bench step's result checked against the reference itself (oracle/_ref,
+    all host cores): same mesh, RHS, Jacobi diagonal and 20 fixed iterations.
+    Runs after the timed regions; the numbers compared are the timed solve's."""
+    import numpy as np
+
+    import oracle
+
+    impl = "reference" if oracle.available("reference") else "oracle"
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    ref = oracle.setup(args.bp, args.degree, (args.elems,) * 3, args.deform, threads=cores,
+                       impl=impl)
+    xr, rep = ref.solve(tol=1e-8, fixed_iterations=args.iters)
+    h_err = oracle.rel_max_diff(rep["residual_history"], np.asarray(history))
+    x_err = oracle.rel_max_diff(xr, np.asarray(x))
+    return {"against": f"{impl} solve_bp, {args.iters} fixed Jacobi-PCG iterations, same workload",
+            "iterations": [len(history) - 1, rep["iterations"]],
+            "residual_history_rel_err": h_err, "x_rel_err": x_err,
+            "ok": bool(h_err <= 1e-10 and x_err <= 1e-10 and len(history) - 1 == rep["iterations"]),
+            "seconds": time.perf_counter() - t0}
 
 
 def run_reference(args):
@@ -236,6 +260,8 @@ def run_reference(args):
                         deform=args.deform, threads=cores)
     iters = args.cpu_iters
     times = []
+    # the reference's pcg timer (pcg.cpp:33-113) — includes its work-vector
+    # allocation, as the reference's own run_bench reports it
     for s in range(args.warmup + args.steps):
         _, rep = prob.solve(tol=1e-8, fixed_iterations=iters)
         if s >= args.warmup:
@@ -249,7 +275,7 @@ def run_reference(args):
         "data": "synthetic (manufactured sin(pi x) sin(pi y) sin(pi z) RHS on the sine-deformed box)",
         "config": {"workload": f"{args.bp} p={args.degree} {args.elems}^3 {args.deform}, "
                                f"Jacobi-PCG {iters} fixed iterations per step",
-                   "n_dofs": prob.n, "threads": cores,
+                   "n_dofs": prob.n, "threads": cores, "same_config": iters == args.iters,
                    "note": "host CPU only; rank 0 runs one per-GPU sub-box sample"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"reference Problem.solve, {iters} fixed CG iterations per "
@@ -313,10 +339,13 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            step()
+            last = step()
         ev1.record(stream)
         torch.cuda.synchronize()
     launches = capi.launch_count() - launches0
+    # the last timed step's result, kept for the check against the reference
+    timed_history = list(last["residual_history"])
+    timed_x = x.cpu().numpy() if world == 1 else None
     # the operator kernel's own duration: the same solve with a CUDA event
     # pair around every K1 launch (kept out of the timed region above: the
     # in-graph event records cost ~7 us each)
@@ -372,6 +401,26 @@ def run_ours(args):
         e2e_ms, t_apply = (float(v) for v in t.tolist())
     e2e_value = n_global * args.iters / (e2e_ms * 1e-3) / 1e9
 
+    # the same public call one solve at a time (no pipelining): H2D(b), solve,
+    # D2H(x) serialised — the latency a single caller sees
+    serial_reps = 5
+    for _ in range(2):
+        prob.pcg_host(bs[0], xs[0], fixed_iterations=args.iters, time_apply=False)
+    torch.cuda.synchronize()
+    barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    s0.record(stream)
+    for _ in range(serial_reps):
+        prob.pcg_host(bs[0], xs[0], fixed_iterations=args.iters, time_apply=False)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    serial_ms = max(s0.elapsed_time(s1), (time.perf_counter() - w0) * 1e3) / serial_reps
+    if world > 1:
+        t = torch.tensor([serial_ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        serial_ms = float(t.item())
+
     if rank != 0:
         return
     peak, peak_kind = measured_peak()
@@ -401,7 +450,14 @@ def run_ours(args):
                      "kernel": op_kernel_name(),
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n_vec,
-                "d2h_bytes_per_step": 8 * n_vec},
+                "d2h_bytes_per_step": 8 * n_vec,
+                "mode": (f"{args.steps} consecutive solves through Problem.pcg_host_batch "
+                         f"(pinned host b in, host x out every solve; copies of neighbouring "
+                         f"solves overlapped with the current one)"),
+                "serial": {"value": n_global * args.iters / (serial_ms * 1e-3) / 1e9,
+                           "ms_per_step": serial_ms,
+                           "mode": "Problem.pcg_host one solve at a time: H2D(b) + solve + "
+                                   "D2H(x) serialised"}},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "setup_seconds": t_setup,
@@ -411,11 +467,17 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(args, sizes)
         except Exception as e:  # report, never fabricate
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+        try:
+            line["verification"] = verify_against_reference(args, timed_history, timed_x)
+        except Exception as e:  # report, never fabricate
+            line["verification"] = {"ok": False, "error": str(e)}
     print(json.dumps(line))
 
 
 def main():
     args = parse()
+    if args.cpu_iters is None:
+        args.cpu_iters = args.iters
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -51,3 +51,22 @@ def test_our_arm_line():
     n_vec = (6 * 7 + 1) ** 3
     assert e["h2d_bytes_per_step"] == 8 * n_vec and e["d2h_bytes_per_step"] == 8 * n_vec
     assert r["gpu_launches"] > 0
+
+
+@pytest.mark.skipif(not oracle.available("reference"), reason="oracle/_ref not built")
+def test_reference_arm_defaults_to_the_same_workload():
+    r = run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--elems", "3")
+    assert r["config"]["same_config"] is True
+    assert "20 fixed iterations" in r["config"]["workload"]
+
+
+@pytest.mark.gpu
+def test_our_arm_verifies_its_timed_result():
+    """With the CPU legs on, the line carries the cpu_baseline and the check of
+    the timed step's residual history and iterate against the reference."""
+    r = run_bench("--steps", "3", "--warmup", "3", "--elems", "5")
+    v = r["verification"]
+    assert v["ok"], v
+    assert v["iterations"] == [20, 20]
+    assert r["cpu_baseline"]["value"] > 0 and r["cpu_baseline"]["cores"] >= 1
+    assert r["e2e"]["serial"]["value"] > 0
