@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "capi_internal.h"
 
 namespace {
@@ -155,6 +157,45 @@ int dmma_warps() {
 }
 
 int max_op_grid() { return num_sms() * 32; }
+
+bool lattice_tma_ok(const OpParams& prm, int m) {
+  static const bool off = [] {
+    const char* v = std::getenv("HXF_TMA");
+    return v && v[0] == '0';
+  }();
+  if (off || !prm.x || prm.idx) return false;
+  if ((reinterpret_cast<uintptr_t>(prm.x) & 15u) != 0) return false;
+  if ((prm.NX * 8) % 16 != 0 || (prm.NX * prm.NY * 8) % 16 != 0) return false;
+  if (m > 1 && (prm.n_L * 8) % 16 != 0) return false;
+  const int64_t lim = int64_t(1) << 31;
+  return prm.NX < lim && prm.NY < lim && prm.NZ < lim && m >= 1 && m <= 3;
+}
+
+bool encode_lattice_map(const OpParams& prm, int m, void* map_out) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return Encode(nullptr);
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[4] = {cuuint64_t(prm.NX), cuuint64_t(prm.NY), cuuint64_t(prm.NZ),
+                              cuuint64_t(m)};
+  const cuuint64_t strides[3] = {cuuint64_t(prm.NX) * 8, cuuint64_t(prm.NX * prm.NY) * 8,
+                                 cuuint64_t(prm.n_L) * 8};
+  const cuuint32_t box[4] = {12, 8, 8, 1};  // 12 columns from an even start (op_dmma.cuh)
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return encode(static_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                const_cast<double*>(prm.x), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 namespace {
 std::atomic<int> g_grid_cap{[] {

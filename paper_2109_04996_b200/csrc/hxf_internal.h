@@ -115,6 +115,15 @@ HXF_DECL_P(16)
 #undef HXF_DECL_P
 
 int num_sms();
+
+// Tensor map (CUtensorMap, 128 bytes) of an operator input viewed as the
+// [m][NZ][NY][NX] f64 lattice with a 12x8x8x1 box (no swizzle), for
+// the TMA gather of the structured-box kernels (encoded through the runtime's
+// driver entry point; no libcuda link).  lattice_tma_ok: whether the lattice
+// and pointer meet TMA's rules (16-byte aligned base, row / plane strides
+// multiples of 16 bytes) and HXF_TMA is not 0.
+bool lattice_tma_ok(const OpParams& prm, int m);
+bool encode_lattice_map(const OpParams& prm, int m, void* map_out);
 // HXF_OP_KERNEL selects the collocated fast path for A/B comparisons:
 // unset/"dmma" -> 0 (tensor-core kernel where available), "pencil" -> 1,
 // "generic" -> 2 (op_kernel.cuh only).

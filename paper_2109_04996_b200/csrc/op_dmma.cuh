@@ -33,17 +33,38 @@
 #ifndef HXF_DMMA_MINB3
 #define HXF_DMMA_MINB3 4
 #endif
+#ifndef HXF_DMMA_TMA_NB  // TMA x slabs per CTA: 2 = issued two work items ahead, 1 = one
+#define HXF_DMMA_TMA_NB 2
+#endif
+#ifndef HXF_DMMA_TMA_MINB  // CTAs per SM the TMA variant's register budget targets
+#define HXF_DMMA_TMA_MINB 4
+#endif
+#ifndef HXF_DMMA_QPF  // elements of geometric factors prefetched into L2 beyond the staged one
+#define HXF_DMMA_QPF 0
+#endif
 #ifndef HXF_DMMA_MINB
 #define HXF_DMMA_MINB 4
 #endif
+#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime's driver entry point)
+
 #include "hxf_device.cuh"
 #include "hxf_internal.h"
 #include "pcg_device.cuh"
 
 namespace hxf {
 
-template <int NC_, int GM_, int NW_ = 4, int NP_ = 8, int NS_ = 1>
+template <int NC_, int GM_, int NW_ = 4, int NP_ = 8, int NS_ = 1, bool TMA_ = false>
 struct DmmaTraits {
+  // TMA: the element's x slab arrives by one tensor-map copy
+  // (cp.async.bulk.tensor.4d over the [m][NZ][NY][NX] lattice, double-
+  // buffered two work items ahead) instead of per-lane loads; structured box
+  // only (GM = 0), lattice rows 16-byte multiples.  A box must start on a
+  // 16-byte boundary (an odd f64 column faults: tools/micro/drv), so the box
+  // is 12 columns wide from the even column at or below the element's first
+  // and the element sits at column offset o = ix0 & 1; 12-double rows keep the
+  // x- and y-direction fragment loads at their 2-wavefront minimum (z: 4)
+  static constexpr bool TMA = TMA_;
+  static_assert(!TMA_ || GM_ == 0, "TMA gather needs the structured box");
   // NS stages of staged geometric factors (1: refill right after the
   // QFunction consumed them; 2: two elements in flight per CTA)
   static constexpr int NS = NS_;
@@ -58,11 +79,18 @@ struct DmmaTraits {
   static_assert(NW_ == 2 || NW_ == 4 || NW_ == 8, "8 planes split over NW warps");
   // CTAs per SM the register budget is sized for (tuned at C3: NW = 4 -> 122
   // registers, 4 CTAs; NW = 2 needs 224 registers to keep its loads in flight)
-  static constexpr int MINB = NW_ == 8 ? 3 : (NC_ == 3 ? HXF_DMMA_MINB3 : HXF_DMMA_MINB);
+  static constexpr int MINB = NW_ == 8 ? 3
+                              : TMA_   ? HXF_DMMA_TMA_MINB
+                                       : (NC_ == 3 ? HXF_DMMA_MINB3 : HXF_DMMA_MINB);
   static constexpr int SLAB = 512;   // doubles
   static constexpr int QDS = 6 * NP3;
-  static constexpr int OFF_QD = 0;
-  static constexpr int OFF_A = NS_ * QDS;  // U, then V0
+  // TMA x buffers first (a TMA destination must be 128-byte aligned)
+  static constexpr int XW = 12, XSLAB = XW * 64;  // box {12, 8, 8, 1}: 6 KB
+  static constexpr int XNB = HXF_DMMA_TMA_NB;
+  static constexpr int OFF_X = 0;
+  static constexpr int XBUF = TMA_ ? XNB * XSLAB : 0;
+  static constexpr int OFF_QD = OFF_X + XBUF;
+  static constexpr int OFF_A = OFF_QD + NS_ * QDS;  // U, then V0
   static constexpr int OFF_B = OFF_A + SLAB;  // V1, then Y2 (dist-Z -> dist-X transpose)
   static constexpr int OFF_Z = OFF_B + SLAB;  // G2, then V2
   static constexpr int SMEM_BYTES = (OFF_Z + SLAB) * 8;
@@ -71,7 +99,22 @@ struct DmmaTraits {
     const int R = j ^ (k & 1);
     return k * 64 + R * 8 + (i ^ (((R >> 1) & 1) << 2));
   }
+  // element point (k, j, i) in a TMA slab whose columns start o before it
+  __device__ static __forceinline__ int tix(int k, int j, int i, int o) {
+    return (k * 8 + j) * XW + o + i;
+  }
 };
+
+// One tensor-map box copy global -> shared (4-D coordinates, innermost
+// first), completion counted on `bar`.
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            int c, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(c), "r"(smem_u32(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -80,12 +123,19 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams prm) {
+__global__ void __launch_bounds__(T::NT, T::MINB)
+    op_dmma_kernel(const __grid_constant__ OpParams prm, const __grid_constant__ CUtensorMap xmap) {
   constexpr int NC = T::NC, P3 = T::P3, NT = T::NT, KK = T::KK;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double dmma_smem[];
+  double* smem = dmma_smem;
   __shared__ __align__(8) uint64_t qbars[T::NS];
+  __shared__ __align__(8) uint64_t xbars[2];
   __shared__ double red_scratch[NT / 32 + 1];
+  double* sX = smem + T::OFF_X;  // TMA: two x slabs (work items q, q+1 / q+2)
 
+  // measurement-only ablation (HXF_ABLATE bit 16): memory traffic and barriers
+  // without the contractions / QFunction arithmetic
+  const bool skipc = (prm.ablate & 16) != 0;
   const int tid = threadIdx.x;
   const int w = tid >> 5, l = tid & 31, g = l >> 2, t = l & 3;
   double* sQD = smem + T::OFF_QD;
@@ -125,10 +175,19 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
   const bool first_qd = (int64_t)blockIdx.x < nsteps && !(prm.ablate & 4);
   if (tid == 0) {
     for (int i = 0; i < T::NS; ++i) mbar_init(&qbars[i], 1);
+    if constexpr (T::TMA) {
+      if (smem_u32(sX) & 127u) __trap();  // TMA destinations are 128-byte aligned
+      mbar_init(&xbars[0], 1);
+      mbar_init(&xbars[1], 1);
+    }
     fence_mbar_init();
     policy = l2_evict_first_policy();
     if (first_qd) {
       issue_qdata(blockIdx.x, 0);
+      for (int d = 1; d <= HXF_DMMA_QPF; ++d)
+        if ((int64_t)blockIdx.x + (T::NS - 1 + d) * G < nsteps)
+          bulk_prefetch_l2(prm.qd + elem(blockIdx.x + (T::NS - 1 + d) * G) * T::QDS,
+                           (uint32_t)(T::QDS * 8));
       if (T::NS > 1 && (int64_t)blockIdx.x + G < nsteps) issue_qdata(blockIdx.x + G, 1);
     }
   }
@@ -148,6 +207,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
     int64_t key;
     uint32_t cmask;
     bool active;
+    int ix0, iy0, iz0;  // element origin on the lattice (TMA box coordinates)
   };
   auto node_of = [&](const Geo& q, int kk, int h) -> int64_t {
     if constexpr (T::GM == 0) return q.key + (int64_t)kk * NXY + h;
@@ -185,6 +245,9 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       const uint32_t ex = e32 - r * (uint32_t)prm.nx, ey = r - ez * (uint32_t)prm.ny;
       const int64_t ix0 = (int64_t)ex * (T::NP - 1), iy0 = (int64_t)ey * (T::NP - 1),
                     iz0 = (int64_t)ez * (T::NP - 1);
+      q.ix0 = (int)ix0;
+      q.iy0 = (int)iy0;
+      q.iz0 = (int)iz0;
       q.key = (ix0 + 2 * t) + prm.NX * (iy0 + g) + NXY * (iz0 + KK * w);
       if (T::GM == 0 && prm.cons_mode == 1) {
         // on_bnd_face per point, as element-face flags x lane masks
@@ -257,13 +320,25 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
 
   Geo gcur = geometry(blockIdx.x);
   Geo gpf = NC > 1 ? gcur : geometry(blockIdx.x + G);
+  // TMA: work item q's slab lands in sX[q & 1], issued two items ahead
+  auto issue_x = [&](const Geo& gq, int c, int buf) {
+    mbar_arrive_expect_tx(&xbars[buf], (uint32_t)(T::XSLAB * 8));
+    tma_load_4d(sX + buf * T::XSLAB, &xmap, gq.ix0 & ~1, gq.iy0, gq.iz0, c, &xbars[buf]);
+  };
   double xn[2 * KK];
-  load_lines(gcur, 0, xn);
   double u[2 * KK];
+  if constexpr (T::TMA) {
+    if (tid == 0) {
+      if (gcur.active) issue_x(gcur, 0, 0);
+      if (T::XNB == 2 && gpf.active) issue_x(gpf, 1 % NC, 1);
+    }
+  } else {
+    load_lines(gcur, 0, xn);
 #pragma unroll
-  for (int m = 0; m < 2 * KK; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
-  store_cons(gcur, 0, xn);
-  load_lines(gpf, 1 % NC, xn);
+    for (int m = 0; m < 2 * KK; ++m) u[m] = (gcur.active && !((gcur.cmask >> m) & 1u)) ? xn[m] : 0.0;
+    store_cons(gcur, 0, xn);
+    load_lines(gpf, 1 % NC, xn);
+  }
   __syncthreads();  // mbarrier init visible
 
   double dot_acc = 0.0;
@@ -274,28 +349,57 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
 #pragma unroll 1
     for (int c = 0; c < NC; ++c, ++q) {
       double* yc = prm.y + c * prm.n_L;
-      // ---- G: this lane's masked dist-X pairs into slab A ----
+      double* X = sX + (q % T::XNB) * T::XSLAB;  // TMA: this item's slab
+      const int xo = gcur.ix0 & 1;          // TMA: the element's column offset in it
+      Geo gnext{};                          // TMA: item q+2 (its slab is issued after (B))
+      const Geo gi1 = gpf;                  // TMA: item q+1 (single-slab variant)
+      if constexpr (T::TMA) {
+        // ---- G: the slab is in shared memory; zero the constrained (and
+        // padding) points in place, storing y = x there first (single apply) ----
+        if (c == NC - 1) gnext_el = gpf;
+        gnext = ((q + 2) / NC == (q + 1) / NC && NC > 1)
+                    ? gpf
+                    : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
+        mbar_wait(&xbars[q % T::XNB], (uint32_t)((q / T::XNB) & 1));
+        if (gcur.cmask) {
 #pragma unroll
-      for (int kk = 0; kk < KK; ++kk)
-        *reinterpret_cast<double2*>(SA + T::off(KK * w + kk, g, 2 * t)) =
-            make_double2(u[2 * kk], u[2 * kk + 1]);
-      // next item's raw lines: land while this item computes
-      {
+          for (int kk = 0; kk < KK; ++kk)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if ((gcur.cmask >> (2 * kk + h)) & 1u) {
+                double* px = X + T::tix(KK * w + kk, g, 2 * t + h, xo);
+                if (!T::PAD && prm.cons_store) yc[node_of(gcur, kk, h)] = *px;
+                *px = 0.0;
+              }
+        }
+        gpf = gnext;
+      } else {
+        // ---- G: this lane's masked dist-X pairs into slab A ----
+#pragma unroll
+        for (int kk = 0; kk < KK; ++kk)
+          *reinterpret_cast<double2*>(SA + T::off(KK * w + kk, g, 2 * t)) =
+              make_double2(u[2 * kk], u[2 * kk + 1]);
+        // next item's raw lines: land while this item computes
         if (c == NC - 1) gnext_el = gpf;  // item q+1 starts the next element
-        const Geo gnext = ((q + 2) / NC == (q + 1) / NC && NC > 1)
-                              ? gpf
-                              : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
+        const Geo gn = ((q + 2) / NC == (q + 1) / NC && NC > 1)
+                           ? gpf
+                           : geometry((int64_t)blockIdx.x + (int64_t)((q + 2) / NC) * G);
         double nx_[2 * KK];
 #pragma unroll
         for (int m = 0; m < 2 * KK; ++m) nx_[m] = xn[m];
         // masked values of item q+1 are formed when it starts (gpf)
-        load_lines(gnext, (q + 2) % NC, xn);
+        load_lines(gn, (q + 2) % NC, xn);
         store_cons(gpf, (q + 1) % NC, nx_);
 #pragma unroll
         for (int m = 0; m < 2 * KK; ++m)
           u[m] = (gpf.active && !((gpf.cmask >> m) & 1u)) ? nx_[m] : 0.0;  // item q+1
-        gpf = gnext;
+        gpf = gn;
       }
+      // forward operand: the TMA slab (swizzled) or slab A
+      auto U = [&](int k, int j, int i) -> double {
+        if constexpr (T::TMA) return X[T::tix(k, j, i, xo)];
+        return SA[T::off(k, j, i)];
+      };
       __syncthreads();  // (A) slab A complete
 
       // ---- forward contractions ----
@@ -306,8 +410,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          dmma(c0, c1, SA[T::off(k, g, 4 * ks + t)], Dr[ks]);  // x: U_k[j][a] . D^T[a][o]
-          dmma(d0, d1, Dr[ks], SA[T::off(k, 4 * ks + t, g)]);  // y: D[o][b] . U_k[b][i]
+          if (!skipc) dmma(c0, c1, U(k, g, 4 * ks + t), Dr[ks]);  // x: U_k[j][a] . D^T[a][o]
+          if (!skipc) dmma(d0, d1, Dr[ks], U(k, 4 * ks + t, g));  // y: D[o][b] . U_k[b][i]
         }
         g0[kk][0] = c0;
         g0[kk][1] = c1;
@@ -319,18 +423,23 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         const int j = KK * w + jj;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dr[ks], SA[T::off(4 * ks + t, j, g)]);
+        for (int ks = 0; ks < 2; ++ks) if (!skipc) dmma(c0, c1, Dr[ks], U(4 * ks + t, j, g));
         *reinterpret_cast<double2*>(SZ + T::off(g, j, 2 * t)) = make_double2(c0, c1);  // dist Z
       }
       const int stg = T::NS > 1 ? (it & 1) : 0;
       const double* sQDs = sQD + stg * T::QDS;
       if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbars[stg], (uint32_t)((it / T::NS) & 1));
-      __syncthreads();  // (B) G2 complete, slab A free
+      if constexpr (T::TMA) fence_proxy_async_smem();  // generic accesses of X before its refill
+      __syncthreads();  // (B) G2 complete, slab A (TMA: this item's x slab) free
+      if constexpr (T::TMA) {
+        if (T::XNB == 2 && tid == 0 && gnext.active) issue_x(gnext, (q + 2) % NC, q & 1);
+        if (T::XNB == 1 && tid == 0 && gi1.active) issue_x(gi1, (q + 1) % NC, 0);
+      }
 
       // ---- QFunction on dist X (qfunction.cpp:135-162) ----
       double energy = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < KK; ++kk) {
+      for (int kk = 0; kk < KK && !skipc; ++kk) {
         const int k = KK * w + kk;
         const int sp = T::off(k, g, 2 * t);
         const double2 z2 = *reinterpret_cast<const double2*>(SZ + sp);
@@ -372,7 +481,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
       if (c == NC - 1) fence_proxy_async_smem();  // generic reads of the factors before the refill
       __syncthreads();  // (C) V0, V1, V2 complete
       if (c == NC - 1 && tid == 0 && e + T::NS * G < nsteps && !(prm.ablate & 4))
+      {
         issue_qdata(e + T::NS * G, stg);
+        // keep DRAM busy one element further ahead: the staged copy of that
+        // element then hits L2
+        const int64_t pf = e + (T::NS + HXF_DMMA_QPF) * G;
+        if (HXF_DMMA_QPF > 0 && pf < nsteps)
+          bulk_prefetch_l2(prm.qd + elem(pf) * T::QDS, (uint32_t)(T::QDS * 8));
+      }
 
       // ---- transposed contractions ----
       double y01[KK][2];
@@ -382,8 +498,8 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
-          dmma(c0, c1, SA[T::off(k, g, 4 * ks + t)], Dc[ks]);  // x^T: V0_k[j][a] . D[a][i]
-          dmma(c0, c1, Dc[ks], SB[T::off(k, 4 * ks + t, g)]);  // y^T: D^T[j][b] . V1_k[b][i]
+          if (!skipc) dmma(c0, c1, SA[T::off(k, g, 4 * ks + t)], Dc[ks]);  // x^T: V0_k[j][a] . D[a][i]
+          if (!skipc) dmma(c0, c1, Dc[ks], SB[T::off(k, 4 * ks + t, g)]);  // y^T: D^T[j][b] . V1_k[b][i]
         }
         y01[kk][0] = c0;
         y01[kk][1] = c1;
@@ -394,7 +510,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmma_kernel(const OpParams 
         const int j = KK * w + jj;
         double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) dmma(c0, c1, Dc[ks], SZ[T::off(4 * ks + t, j, g)]);  // z^T
+        for (int ks = 0; ks < 2; ++ks) if (!skipc) dmma(c0, c1, Dc[ks], SZ[T::off(4 * ks + t, j, g)]);  // z^T
         y2z[jj][0] = c0;
         y2z[jj][1] = c1;
       }

@@ -129,8 +129,12 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   const int grid = capped_grid(prm.E, max_ctas);
   if (grid_out) *grid_out = grid;
   if (grid == 0) return cudaSuccess;
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof xmap);
+  if constexpr (T::TMA)
+    if (!encode_lattice_map(prm, T::NC, &xmap)) return cudaErrorInvalidValue;
   const cudaError_t err = launch_pdl_if(pdl_enabled() || prm.pdl, kern, dim3(grid), dim3(T::NT),
-                                        T::SMEM_BYTES, s, prm);
+                                        T::SMEM_BYTES, s, prm, xmap);
   count_launch();
   return err;
 }
@@ -143,7 +147,12 @@ cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
       return run_dmma<DmmaTraits<NC, 1, NW, NP, 2>>(prm, s, g);
     }
   }
-  if (!prm.idx && prm.cons_mode != 2) return run_dmma<DmmaTraits<NC, 0, NW, NP>>(prm, s, g);
+  if (!prm.idx && prm.cons_mode != 2) {
+    // structured box: the x slab by tensor-map TMA where the lattice allows it
+    if constexpr (NW == 4)
+      if (lattice_tma_ok(prm, NC)) return run_dmma<DmmaTraits<NC, 0, NW, NP, 1, true>>(prm, s, g);
+    return run_dmma<DmmaTraits<NC, 0, NW, NP>>(prm, s, g);
+  }
   return run_dmma<DmmaTraits<NC, 1, NW, NP>>(prm, s, g);
 }
 

@@ -112,7 +112,7 @@ def test_python_api_surface_matches_oracle():
     assert np.array_equal(out, oracle.apply_basis(4, "gauss", 6, "grad", "transpose", 3, ub))
     M = np.arange(1.0, 5.0)
     v, fl = _core.contract_batch(M, 2, 2, 0, (2, 2, 2), 1, np.arange(1.0, 9.0))
-    assert list(v[:4]) == [5, 11, 11, 25] and fl == 16
+    assert list(v[:4]) == [5, 11, 11, 25] and fl == 2 * 8 * 2
     assert _core.flops_estimate(1, 1, 1, "grad") == 84
     prob = hx.setup("bp6", degree=2, dims=(3, 2, 2), deform="sine")
     ref = oracle.setup("bp6", 2, (3, 2, 2), "sine")
