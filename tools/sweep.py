@@ -51,6 +51,27 @@ def sizes_for(bp, p, d):
     return n, ba, ba + 88 * m * n1 ** 3
 
 
+def flops_apply(bp, p, d):
+    """Algorithmic FP64 flops of one fused apply: per element
+    and component, BP5/6 12 P^4 + 15 P^3; BP3/4 4 (I + 3 q^4) + 15 q^3; BP1/2
+    4 I + q^3, with I = q P^3 + q^2 P^2 + q^3 P (P = p+1)."""
+    k = int(bp[2])
+    m = 1 if k % 2 == 1 else 3
+    P = p + 1
+    q = p + 2 if k <= 4 else p + 1
+    interp = q * P ** 3 + q * q * P * P + q ** 3 * P
+    if k >= 5:
+        f = 12 * P ** 4 + 15 * P ** 3
+    elif k >= 3:
+        f = 4 * (interp + 3 * q ** 4) + 15 * q ** 3
+    else:
+        f = 4 * interp + q ** 3
+    return f * m * d ** 3
+
+
+FP64_PEAK_TFS = 37.0  # DMMA m8n8k4 rate measured on this B200 (tools/micro/fp64_rate.cu)
+
+
 def pick_d(bp, p, target):
     best = None
     for d in range(1, 2000):
@@ -119,7 +140,8 @@ def main():
                        apply_gdofs=n / t_apply / 1e9, apply_frac=bapply / t_apply / 1e9 / peak,
                        k1_us=k1 * 1e6, k1_frac=bapply / k1 / 1e9 / peak,
                        cg_us=t_it * 1e6, cg_gdofs=n / t_it / 1e9,
-                       cg_frac=bcg / t_it / 1e9 / peak, setup_s=tsetup)
+                       cg_frac=bcg / t_it / 1e9 / peak, setup_s=tsetup,
+                       k1_tflops=flops_apply(a.bp, p, d) / k1 / 1e12)
             if a.cpu:
                 import os
 
@@ -152,13 +174,14 @@ def main():
                     f"HBM peak {peak} GB/s measured)\n\n")
             cpu = a.cpu and rows
             f.write("| p | d | n (DOFs) | apply us | apply GDOF/s | apply roof | K1 us | K1 roof "
-                    "| CG us/iter | CG GDOF/s | CG roof |" +
+                    "| K1 FP64 TF/s (of 37) | CG us/iter | CG GDOF/s | CG roof |" +
                     (f" ref CPU GDOF/s ({rows[0]['cpu_cores']} thr) | CG speed-up |" if cpu else "") +
-                    "\n|---|---|---|---|---|---|---|---|---|---|---|" + ("---|---|" if cpu else "") + "\n")
+                    "\n|---|---|---|---|---|---|---|---|---|---|---|---|" + ("---|---|" if cpu else "") + "\n")
             for r in rows:
                 f.write(f"| {r['p']} | {r['d']} | {r['n']:,} | {r['apply_us']:.1f} | "
                         f"{r['apply_gdofs']:.2f} | {r['apply_frac']:.2f} | {r['k1_us']:.1f} | "
-                        f"{r['k1_frac']:.2f} | {r['cg_us']:.1f} | {r['cg_gdofs']:.2f} | "
+                        f"{r['k1_frac']:.2f} | {r['k1_tflops']:.1f} ({r['k1_tflops'] / FP64_PEAK_TFS:.2f}) | "
+                        f"{r['cg_us']:.1f} | {r['cg_gdofs']:.2f} | "
                         f"{r['cg_frac']:.2f} |" +
                         (f" {r['cpu_gdofs']:.4f} | {r['cg_gdofs'] / r['cpu_gdofs']:.0f}x |" if cpu else "") +
                         "\n")
