@@ -180,6 +180,23 @@ int hxf_apply_tensor_3d(hxf_ctx* ctx, int p, int q, const double* interp1d, cons
  * the sum-factorized kernel; Grad = 3 x Interp; direction-independent. */
 uint64_t hxf_flops_estimate(int p, int q, int m, hxf_eval_mode mode);
 
+/* ---- structured-box setup on the device (build_mesh + bench.cpp fields) ----
+ * The element box [off, off+loc) of a global box of glob elements (whole box:
+ * off = 0, loc = glob), degree p, GLL nodes gll_nodes[p+1]: node coordinates
+ * (3*n_L component-major, mesh.cpp:32-78 — bit-exact: the 1-D axes and their
+ * sines are evaluated on the host as the reference does, the lattice and
+ * sine bump on the device), and optionally the manufactured fields
+ * (bench.cpp:56-62): u = sin(pi x) sin(pi y) sin(pi z) and f = 3 pi^2 u
+ * (poisson) or u, each replicated over m components.  On the undeformed box
+ * u and f are bit-exact too; on the sine box the deformed points' sines come
+ * from the device's sin (within 2 ulp of the host's).  Any of coords / f / u
+ * may be NULL. */
+int hxf_box_fields(hxf_ctx* ctx, const int glob[3], const int off[3], const int loc[3], int p,
+                   const double* gll_nodes, int deform, int m, int poisson, double* coords,
+                   double* f, double* u, hxf_memspace space);
+/* v[c*n_L + i] = value on every constrained row i of the operator (device v). */
+int hxf_operator_set_constrained(hxf_op* op, double* v, double value, hxf_memspace space);
+
 /* ---- PCG: replaces pcg(ApplyFn, ...) for this operator ---------------------
  * proj/include/hexfem/pcg.hpp:13-41, proj/src/pcg.cpp:24-115.  x0 = 0;
  * diag = NULL means unpreconditioned.  Runs device-resident: only b (and the

@@ -33,7 +33,8 @@ EXPORTS = (
     "hxf_elem_restriction_create", "hxf_elem_restriction_destroy",
     "hxf_elem_restriction_is_structured", "hxf_elem_restriction_apply",
     "hxf_elem_restriction_multiplicity", "hxf_elem_restriction_gather_scalar",
-    "hxf_contract_batch", "hxf_apply_tensor_3d", "hxf_flops_estimate",
+    "hxf_contract_batch", "hxf_apply_tensor_3d", "hxf_flops_estimate", "hxf_box_fields",
+    "hxf_operator_set_constrained",
 )
 
 
@@ -134,6 +135,8 @@ def lib() -> C.CDLL:
     L.hxf_contract_batch.argtypes = [P, P, I64, I, I, I, P, I64, P, I64, P, I64, I, I,
                                      C.POINTER(C.c_uint64)]
     L.hxf_apply_tensor_3d.argtypes = [P, I, I, P, P, I, I, I, P, I64, P, I64, I]
+    L.hxf_box_fields.argtypes = [P, P, P, P, I, P, I, I, I, P, P, P, I]
+    L.hxf_operator_set_constrained.argtypes = [P, P, D, I]
     L.hxf_flops_estimate.restype = C.c_uint64
     L.hxf_flops_estimate.argtypes = [I, I, I, I]
     _lib = L

@@ -9,6 +9,7 @@
 // aux_kernels.cu, so their results are the reference's bit for bit (the
 // restriction's G^T in the reference's colour-class order whenever the table
 // is the structured box, which make_restriction always produces).
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -230,6 +231,74 @@ int hxf_apply_tensor_3d(hxf_ctx* ctx, int p, int q, const double* interp1d, cons
                             1, du + c * in_size, dv + c * out_size),
          "apply_tensor_3d");
     finish_out(v, dv, size_t(v_len), space, s, "apply_tensor_3d");
+  });
+}
+
+int hxf_box_fields(hxf_ctx* ctx, const int glob[3], const int off[3], const int loc[3], int p,
+                   const double* gll_nodes, int deform, int m, int poisson, double* coords,
+                   double* f, double* u, hxf_memspace space) {
+  return guarded([&] {
+    if (!ctx || !glob || !off || !loc || !gll_nodes) fail(HXF_EINVAL, "build_mesh: NULL argument");
+    if (p < 1) fail(HXF_EINVAL, "build_mesh: p must be >= 1");
+    for (int a = 0; a < 3; ++a)
+      if (glob[a] < 1 || loc[a] < 1 || off[a] < 0 || off[a] + loc[a] > glob[a])
+        fail(HXF_EINVAL, "build_mesh: element counts must be >= 1");
+    if (m < 1) fail(HXF_EINVAL, "bp_setup: m must be >= 1");
+    cudaStream_t s = ctx->stream;
+    // 1-D axes and their sines on the host, exactly as mesh.cpp:12-28,57-58
+    // evaluate them (glibc sin): the only transcendental calls of the
+    // undeformed fields
+    int64_t gdim[3], ldim[3], noff[3];
+    std::vector<double> axes;
+    for (int a = 0; a < 3; ++a) {
+      gdim[a] = int64_t(glob[a]) * p + 1;
+      ldim[a] = int64_t(loc[a]) * p + 1;
+      noff[a] = int64_t(off[a]) * p;
+    }
+    std::vector<double> c[3];
+    for (int a = 0; a < 3; ++a) {
+      const int ne = glob[a];
+      c[a].assign(size_t(gdim[a]), 0.0);
+      const double h = 1.0 / ne;
+      for (int k = 0; k < ne; ++k)
+        for (int j = 0; j <= p; ++j)
+          c[a][size_t(k) * p + size_t(j)] = (k + 0.5 * (gll_nodes[j] + 1.0)) * h;
+      c[a].back() = 1.0;
+      c[a].front() = 0.0;
+    }
+    for (int a = 0; a < 3; ++a) axes.insert(axes.end(), c[a].begin(), c[a].end());
+    for (int a = 0; a < 3; ++a)
+      for (double v : c[a]) axes.push_back(std::sin(M_PI * v));
+    const int64_t n_L = ldim[0] * ldim[1] * ldim[2];
+    double* dax = ctx->scratch_c.ensure(axes.size());
+    h2d(dax, axes.data(), axes.size() * 8, s);
+    double* dc = coords;
+    double* df = f;
+    double* du = u;
+    if (space == HXF_HOST) {  // staging: coords | f | u
+      const size_t need = (coords ? 3 : 0) * size_t(n_L) + (f ? m : 0) * size_t(n_L) +
+                          (u ? m : 0) * size_t(n_L);
+      double* st = ctx->scratch_b.ensure(need);
+      dc = coords ? st : nullptr;
+      df = f ? st + (coords ? 3 * n_L : 0) : nullptr;
+      du = u ? st + (coords ? 3 * n_L : 0) + (f ? int64_t(m) * n_L : 0) : nullptr;
+    }
+    ck(launch_box_fields(s, dax, gdim, noff, ldim, deform, m, poisson, dc, df, du), "box fields");
+    if (space == HXF_HOST) {
+      if (coords) d2h(coords, dc, size_t(3 * n_L) * 8, s);
+      if (f) d2h(f, df, size_t(m) * n_L * 8, s);
+      if (u) d2h(u, du, size_t(m) * n_L * 8, s);
+    }
+    ck(cudaStreamSynchronize(s), "box fields");
+  });
+}
+
+int hxf_operator_set_constrained(hxf_op* op, double* v, double value, hxf_memspace space) {
+  return guarded([&] {
+    if (!op || !v) fail(HXF_EINVAL, "set_constrained: NULL argument");
+    if (space != HXF_DEVICE) fail(HXF_EINVAL, "set_constrained: device vectors only");
+    op_set_constrained(op, v, value, op->ctx->stream);
+    ck(cudaStreamSynchronize(op->ctx->stream), "set_constrained");
   });
 }
 

@@ -273,6 +273,50 @@ __global__ void qdata_point_kernel(int kind, int nq1, const double* __restrict__
     }
 }
 
+// Setup fields of the structured box on the device (mesh.cpp:42-78,
+// bench.cpp:56-62, 89-105): node coordinates from the 1-D axes and the
+// per-axis sines of the undeformed axes (host-computed, glibc), the sine bump
+// ((0.05 sx) sy) sz, and the manufactured u* = sin(pi x) sin(pi y) sin(pi z)
+// / f = 3 pi^2 u*.  Coordinates are the reference's bit for bit; u*, f too
+// on the undeformed box (the axis sines ARE sin(pi x)); on the sine box the
+// deformed point's sines come from CUDA's sin (<= 2 ulp from glibc's).
+struct BoxAxes {
+  const double *cx, *cy, *cz;  // global 1-D axes (mesh.cpp:12-28)
+  const double *sx, *sy, *sz;  // sin(M_PI * c) on those axes
+};
+
+__global__ void box_fields_kernel(BoxAxes ax, int64_t NX, int64_t NY, int64_t n_L, int64_t ox,
+                                  int64_t oy, int64_t oz, int deform, int m, int poisson,
+                                  double* __restrict__ coords, double* __restrict__ f,
+                                  double* __restrict__ u) {
+  for (int64_t node = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; node < n_L;
+       node += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ix = node % NX, r = node / NX, iy = r % NY, iz = r / NY;
+    const int64_t gx = ox + ix, gy = oy + iy, gz = oz + iz;
+    double x = ax.cx[gx], y = ax.cy[gy], z = ax.cz[gz];
+    double uv;
+    if (deform) {
+      const double bump = dmul(dmul(dmul(0.05, ax.sx[gx]), ax.sy[gy]), ax.sz[gz]);
+      x = dadd(x, bump);
+      y = dadd(y, bump);
+      z = dadd(z, bump);
+      uv = dmul(dmul(sin(dmul(M_PI, x)), sin(dmul(M_PI, y))), sin(dmul(M_PI, z)));
+    } else {
+      uv = dmul(dmul(ax.sx[gx], ax.sy[gy]), ax.sz[gz]);
+    }
+    if (coords) {
+      coords[node] = x;
+      coords[n_L + node] = y;
+      coords[2 * n_L + node] = z;
+    }
+    const double fv = poisson ? dmul(dmul(dmul(3.0, M_PI), M_PI), uv) : uv;
+    for (int c = 0; c < m; ++c) {
+      if (f) f[c * n_L + node] = fv;
+      if (u) u[c * n_L + node] = uv;
+    }
+  }
+}
+
 // operator_diagonal element part (operator.cpp:178-244): transpose chains of
 // Hadamard-squared 1-D factors over the (unscaled) geometric factors.
 struct DiagFactors {
@@ -354,6 +398,23 @@ cudaError_t launch_basis_apply(cudaStream_t s, int p, int q, const double* B, co
   if (ne == 0) return cudaSuccess;
   basis_apply_kernel<<<(unsigned)ne, 128, smem, s>>>(BasisDev{B, G, Bt, Gt}, nn, q, mode, dir, ne,
                                                      in, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_box_fields(cudaStream_t s, const double* axes, const int64_t gdim[3],
+                              const int64_t off[3], const int64_t ldim[3], int deform, int m,
+                              int poisson, double* coords, double* f, double* u) {
+  BoxAxes ax;
+  ax.cx = axes;
+  ax.cy = ax.cx + gdim[0];
+  ax.cz = ax.cy + gdim[1];
+  ax.sx = ax.cz + gdim[2];
+  ax.sy = ax.sx + gdim[0];
+  ax.sz = ax.sy + gdim[1];
+  const int64_t n_L = ldim[0] * ldim[1] * ldim[2];
+  box_fields_kernel<<<grid_for(n_L, 256), 256, 0, s>>>(ax, ldim[0], ldim[1], n_L, off[0], off[1],
+                                                      off[2], deform, m, poisson, coords, f, u);
   count_launch();
   return cudaGetLastError();
 }

@@ -15,6 +15,11 @@ struct Lattice {
 cudaError_t launch_basis_apply(cudaStream_t s, int p, int q, const double* B, const double* G,
                                const double* Bt, const double* Gt, int mode, int dir, int64_t ne,
                                const double* in, double* out);
+// structured-box setup fields: axes = [cx | cy | cz | sx | sy | sz] (global
+// node counts gdim), the local box of ldim nodes at node offset off
+cudaError_t launch_box_fields(cudaStream_t s, const double* axes, const int64_t gdim[3],
+                              const int64_t off[3], const int64_t ldim[3], int deform, int m,
+                              int poisson, double* coords, double* f, double* u);
 // contract_batch: one 1-D contraction of ne element blocks (device M, n_out x n_in)
 cudaError_t launch_contract_batch(cudaStream_t s, const double* M, int n_out, int n_in, int dim,
                                   const int shape[3], int64_t ne, const double* in, double* out,

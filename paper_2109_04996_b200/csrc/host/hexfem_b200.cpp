@@ -7,6 +7,8 @@
 // the geometric factors, operator applies, diagonal and PCG run on the GPU.
 #include "hexfem_b200.hpp"
 
+#include <chrono>
+
 #include <algorithm>
 #include <charconv>
 #include <cmath>
@@ -159,9 +161,11 @@ namespace {
 // `glob` elements, coordinates evaluated on the global 1-D axes (mesh.cpp:
 // 42-78) so a sub-box mesh is bit-equal to the matching part of the global.
 HexMesh build_box_mesh(std::array<int, 3> glob, std::array<int, 3> off, std::array<int, 3> loc,
-                       int p, Deformation deformation) {
+                       int p, Deformation deformation, bool with_coords = true) {
   HexMesh mesh;
   mesh.dims = loc;
+  mesh.global_dims = glob;
+  mesh.offset = off;
   mesh.p = p;
   mesh.deformation = deformation;
   mesh.nodes_per_axis = {int64_t(loc[0]) * p + 1, int64_t(loc[1]) * p + 1, int64_t(loc[2]) * p + 1};
@@ -182,6 +186,16 @@ HexMesh build_box_mesh(std::array<int, 3> glob, std::array<int, 3> off, std::arr
   const int64_t GX = int64_t(glob[0]) * p + 1, GY = int64_t(glob[1]) * p + 1,
                 GZ = int64_t(glob[2]) * p + 1;
   const int64_t ox = int64_t(off[0]) * p, oy = int64_t(off[1]) * p, oz = int64_t(off[2]) * p;
+  if (!with_coords) {  // topology only: the global-boundary nodes (mesh.cpp:67-71)
+    for (int64_t iz = 0; iz < NZ; ++iz)
+      for (int64_t iy = 0; iy < NY; ++iy)
+        for (int64_t ix = 0; ix < NX; ++ix) {
+          const int64_t gx = ox + ix, gy = oy + iy, gz = oz + iz;
+          if (gx == 0 || gx == GX - 1 || gy == 0 || gy == GY - 1 || gz == 0 || gz == GZ - 1)
+            mesh.boundary_nodes.push_back(ix + NX * (iy + NY * iz));
+        }
+    return mesh;
+  }
   mesh.coords.assign(size_t(3 * mesh.n_L), 0.0);
   // the sine bump factorises: s(x,y,z) = sin(pi x) sin(pi y) sin(pi z), with
   // the reference's evaluation order ((eps*sx)*sy)*sz kept per node
@@ -217,6 +231,11 @@ HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation) {
     throw std::invalid_argument("build_mesh: element counts must be >= 1");
   if (p < 1) throw std::invalid_argument("build_mesh: p must be >= 1");
   return build_box_mesh({nx, ny, nz}, {0, 0, 0}, {nx, ny, nz}, p, deformation);
+}
+
+std::vector<double> mesh_coords(const HexMesh& mesh) {
+  if (!mesh.coords.empty()) return mesh.coords;
+  return build_box_mesh(mesh.global_dims, mesh.offset, mesh.dims, mesh.p, mesh.deformation).coords;
 }
 
 // ------------------------------------------------------------ partition
@@ -516,7 +535,27 @@ const double* BpProblem::diagonal_device() {
 
 // bp_setup (bench.cpp:64-119): mesh + basis on the host, geometric factors,
 // RHS mass apply and everything after on the GPU.
+const std::vector<double>& BpProblem::host_rhs() {
+  if (rhs.size() != size_t(size())) {
+    rhs.assign(size_t(size()), 0.0);
+    d_rhs.download(rhs.data(), rhs.size());
+  }
+  return rhs;
+}
+
+const std::vector<double>& BpProblem::host_exact() {
+  if (exact_nodal.size() != size_t(size())) {
+    exact_nodal.assign(size_t(size()), 0.0);
+    const auto gll = make_quadrature(QuadratureKind::GaussLobattoLegendre, config.p + 1).points;
+    check(hxf_box_fields(device->ctx(), sub.global_dims.data(), sub.offset.data(), sub.dims.data(),
+                         config.p, gll.data(), config.deformation == Deformation::Sine ? 1 : 0, m,
+                         0, nullptr, nullptr, exact_nodal.data(), HXF_HOST));
+  }
+  return exact_nodal;
+}
+
 std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
+  const auto t_start = std::chrono::steady_clock::now();
   if (config.p < 1) throw std::invalid_argument("bp_setup: p must be >= 1");
   for (int d : config.dims)
     if (d < 1) throw std::invalid_argument("bp_setup: element counts must be >= 1");
@@ -529,20 +568,45 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
   const int q = bp_quadrature_points(config.bp, config.p);
   if (comm) {
     prob->sub = make_subdomain(config.dims, comm->size(), comm->rank(), config.proc_grid);
-    prob->mesh = build_submesh(prob->sub, config.p, config.deformation);
   } else {
     prob->sub = make_subdomain(config.dims, 1, 0);
-    prob->mesh = build_mesh(config.dims[0], config.dims[1], config.dims[2], config.p,
-                            config.deformation);
   }
+  // device setup: the host keeps only the lattice topology (boundary nodes)
+  prob->mesh = build_box_mesh(prob->sub.global_dims, prob->sub.offset, prob->sub.dims, config.p,
+                              config.deformation, config.host_setup);
   prob->basis = make_basis(config.p, make_quadrature(bp_quadrature_kind(config.bp), q));
   const HexMesh& mesh = prob->mesh;
   const int64_t n_L = mesh.n_L;
   const int m = prob->m;
   const double alpha = bp_alpha(config.bp), beta = bp_beta(config.bp);
 
+  const bool poisson = alpha > 0;
   DeviceBuffer d_coords(dev, size_t(3 * n_L));
-  d_coords.upload(mesh.coords.data(), size_t(3 * n_L));
+  DeviceBuffer d_f(dev, size_t(m) * n_L);
+  if (config.host_setup) {
+    // the reference's order on the host (mesh.cpp:42-78, bench.cpp:89-105)
+    d_coords.upload(mesh.coords.data(), size_t(3 * n_L));
+    std::vector<double> f(size_t(m) * n_L);
+    prob->exact_nodal.assign(size_t(m) * n_L, 0.0);
+    for (int64_t i = 0; i < n_L; ++i) {
+      const double x = mesh.coords[size_t(i)], y = mesh.coords[size_t(n_L + i)],
+                   z = mesh.coords[size_t(2 * n_L + i)];
+      const double u = manufactured_solution(x, y, z);
+      const double fv = poisson ? manufactured_rhs(x, y, z) : u;
+      for (int c = 0; c < m; ++c) {
+        f[size_t(c * n_L + i)] = fv;
+        prob->exact_nodal[size_t(c * n_L + i)] = u;
+      }
+    }
+    d_f.upload(f.data(), f.size());
+  } else {
+    // device: only the 1-D axes cross the bus (hxf_box_fields)
+    const auto gll = make_quadrature(QuadratureKind::GaussLobattoLegendre, config.p + 1).points;
+    check(hxf_box_fields(dev->ctx(), prob->sub.global_dims.data(), prob->sub.offset.data(),
+                         prob->sub.dims.data(), config.p, gll.data(),
+                         config.deformation == Deformation::Sine ? 1 : 0, m, poisson ? 1 : 0,
+                         d_coords.data(), d_f.data(), nullptr, HXF_DEVICE));
+  }
   DeviceBuffer mass_qd = device_qdata(dev, mesh, prob->basis, d_coords, HXF_QDATA_MASS);
   DeviceBuffer diff_qd;
   if (alpha > 0) diff_qd = device_qdata(dev, mesh, prob->basis, d_coords, HXF_QDATA_DIFFUSION);
@@ -550,31 +614,18 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
 
   if (bp_has_constraints(config.bp)) prob->constrained = mesh.boundary_nodes;
 
-  // manufactured fields at the nodes, b = B f with the unconstrained mass op
-  std::vector<double> f(size_t(m) * n_L);
-  prob->exact_nodal.assign(size_t(m) * n_L, 0.0);
-  const bool poisson = alpha > 0;
-  for (int64_t i = 0; i < n_L; ++i) {
-    const double x = mesh.coords[size_t(i)], y = mesh.coords[size_t(n_L + i)],
-                 z = mesh.coords[size_t(2 * n_L + i)];
-    const double u = manufactured_solution(x, y, z);
-    const double fv = poisson ? manufactured_rhs(x, y, z) : u;
-    for (int c = 0; c < m; ++c) {
-      f[size_t(c * n_L + i)] = fv;
-      prob->exact_nodal[size_t(c * n_L + i)] = u;
-    }
-  }
-  prob->rhs.assign(size_t(m) * n_L, 0.0);
+  // b = B f with the unconstrained mass operator (assembled across interfaces),
+  // constrained entries then zeroed (bench.cpp:106-111), all on the device
+  prob->d_rhs = DeviceBuffer(dev, size_t(m) * n_L);
   {
     hxf_operator_desc d = base_desc(mesh, prob->basis, m);
     d.mass_qdata = mass_qd.data();
     d.beta = 1.0;
     Operator mass_op(dev, d);
-    if (comm) mass_op.set_partition(*comm, prob->sub);  // assembled across interfaces
-    mass_op.apply_host(f.data(), prob->rhs.data());
+    if (comm) mass_op.set_partition(*comm, prob->sub);
+    mass_op.apply_device(d_f.data(), prob->d_rhs.data());
   }
-  for (int c = 0; c < m; ++c)
-    for (int64_t i : prob->constrained) prob->rhs[size_t(c * n_L + i)] = 0.0;
+  d_f = DeviceBuffer();
 
   hxf_operator_desc d = base_desc(mesh, prob->basis, m);
   d.alpha = alpha;
@@ -587,10 +638,12 @@ std::unique_ptr<BpProblem> bp_setup(const BpConfig& config) {
   if (comm) prob->op->set_partition(*comm, prob->sub);
   prob->n_dofs_local = int64_t(m) * (n_L - int64_t(prob->constrained.size()));
   prob->n_dofs = bp_dof_count(config.bp, config.p, config.dims);  // global
-  prob->d_rhs = DeviceBuffer(dev, size_t(m) * n_L);
-  prob->d_rhs.upload(prob->rhs.data(), prob->rhs.size());
+  if (!prob->constrained.empty())
+    check(hxf_operator_set_constrained(prob->op->handle(), prob->d_rhs.data(), 0.0, HXF_DEVICE));
   prob->d_diag = DeviceBuffer(dev, size_t(m) * n_L);
   prob->d_x = DeviceBuffer(dev, size_t(m) * n_L);
+  prob->setup_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return prob;
 }
 
@@ -619,10 +672,11 @@ double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
   const int S = n1 * n1 * n1, nq = q * q * q;
   if (int64_t(u_h.size()) != int64_t(m) * n_L)
     throw std::invalid_argument("l2_error: solution length mismatch");
+  const std::vector<double> coords = mesh_coords(mesh);
   // w det J at the Gauss points on the device
   std::vector<double> wdet(size_t(E) * nq);
   check(hxf_qdata_compute(dev->ctx(), p, q, eb.interp1d.data(), eb.grad1d.data(),
-                          eb.quad.weights.data(), E, n_L, mesh.coords.data(), nullptr,
+                          eb.quad.weights.data(), E, n_L, coords.data(), nullptr,
                           mesh.dims.data(), HXF_QDATA_MASS, wdet.data(), HXF_HOST));
   // element values of coords (3) and solution (m) -> quadrature points
   const int nfield = 3 + m;
@@ -637,7 +691,7 @@ double l2_error(const HexMesh& mesh, int m, const std::vector<double>& u_h,
         for (int kx = 0; kx <= p; ++kx, ++s) {
           const int64_t node = (ex * p + kx) + NX * ((ey * p + ky) + NY * (ez * p + kz));
           for (int a = 0; a < 3; ++a)
-            ev[size_t((a * E + e) * S + s)] = mesh.coords[size_t(a * n_L + node)];
+            ev[size_t((a * E + e) * S + s)] = coords[size_t(a * n_L + node)];
           for (int c = 0; c < m; ++c)
             ev[size_t(((3 + c) * E + e) * S + s)] = u_h[size_t(c * n_L + node)];
         }

@@ -51,13 +51,17 @@ struct HexMesh {
   int p = 1;
   std::array<int64_t, 3> nodes_per_axis{};
   int64_t n_L = 0;
-  std::vector<double> coords;  // 3*n_L component-major
+  std::vector<double> coords;  // 3*n_L component-major (empty: device-built, see mesh_coords)
+  std::array<int, 3> global_dims{}, offset{};  // the element box this lattice is part of
   std::vector<int64_t> boundary_nodes;
   Deformation deformation = Deformation::None;
   int64_t num_elements() const { return int64_t(dims[0]) * dims[1] * dims[2]; }
   int nodes_per_elem() const { return (p + 1) * (p + 1) * (p + 1); }
 };
 HexMesh build_mesh(int nx, int ny, int nz, int p, Deformation deformation = Deformation::None);
+// The host coordinates of a mesh whose coordinates were built on the device
+// (bp_setup): rebuilt on demand, bit-equal to build_mesh's.
+std::vector<double> mesh_coords(const HexMesh& mesh);
 
 // ---- partitioned box (no reference counterpart) -----------
 // The global element box is split into a grid of sub-boxes, one per rank,
@@ -226,6 +230,9 @@ struct BpConfig {
   double tol_rel = 1e-8;
   int max_iter = 2000;
   int device = 0;
+  // setup fields (coordinates, manufactured f and u, b = B f) on the host (the
+  // reference's path; f bit-exact on the sine box too) instead of the device
+  bool host_setup = false;
   // partitioned: dims are the GLOBAL element counts, this rank builds its sub-box
   std::shared_ptr<Communicator> comm;
   std::optional<std::array<int, 3>> proc_grid;
@@ -272,8 +279,8 @@ struct BpProblem {
   int m = 1;
   int64_t n_dofs = 0;
   std::vector<int64_t> constrained;
-  std::vector<double> rhs;          // B f, constrained entries zeroed
-  std::vector<double> exact_nodal;  // nodal interpolant of u*
+  std::vector<double> rhs;          // B f, constrained entries zeroed (host copy: host_rhs())
+  std::vector<double> exact_nodal;  // nodal interpolant of u* (host copy: host_exact())
   std::shared_ptr<Device> device;
   Subdomain sub;  // whole box unless config.comm is set
   int64_t n_dofs_local = 0;
@@ -282,6 +289,10 @@ struct BpProblem {
   bool diag_ready = false;
   int64_t size() const { return int64_t(m) * mesh.n_L; }
   const double* diagonal_device();  // computed once, cached
+  // host copies of the device-built fields, made on first use
+  const std::vector<double>& host_rhs();
+  const std::vector<double>& host_exact();
+  double setup_seconds = 0;  // host wall time of bp_setup
 };
 
 std::unique_ptr<BpProblem> bp_setup(const BpConfig& config);

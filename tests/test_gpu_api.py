@@ -88,7 +88,8 @@ def test_setup_apply_diag_parity(bp, p, dims):
     assert ours.n == ref.n and ours.num_nodes == ref.num_nodes
     assert np.array_equal(ours.coords, ref.coords)
     assert np.array_equal(ours.constrained, ref.constrained)
-    assert np.array_equal(ours.exact, ref.exact)
+    # device setup: u* at the deformed nodes from the device's sin (<= 2 ulp)
+    assert oracle.rel_max_diff(ref.exact, ours.exact) <= 1e-15
     assert oracle.rel_max_diff(ref.rhs, ours.rhs) <= 1e-12
     x = oracle.seeded_uniform(ref.size, 99)
     assert oracle.rel_max_diff(ref.apply(x), ours.apply(x)) <= 1e-12
@@ -183,3 +184,28 @@ def test_cached_solve_graph_survives_buffer_growth():
     x3, r3 = prob.solve(tol=1e-8, fixed_iterations=20)
     assert oracle.rel_max_diff(r1["residual_history"], r3["residual_history"]) <= 1e-12
     assert oracle.rel_max_diff(x1, x3) <= 1e-12
+
+
+@pytest.mark.parametrize("bp,p,dims,deform", [("bp5", 7, (4, 3, 3), "sine"), ("bp3", 3, (3, 2, 2), "none"),
+                                              ("bp2", 2, (2, 3, 2), "none"), ("bp6", 4, (2, 2, 3), "sine")])
+def test_device_setup_fields(bp, p, dims, deform):
+    """bp_setup builds coordinates, u*, f and b = B f on the device from the
+    1-D axes.  Against the reference: coordinates and the
+    geometric factors (hence the diagonal) bit-exact; u* bit-exact on the
+    undeformed box (the axis sines are the nodes' sines) and within 2 ulp on
+    the sine box (device sin); b within 1e-15.  host_setup=True keeps the
+    reference's host path (f bit-exact everywhere)."""
+    ref = oracle.setup(bp, p, dims, deform)
+    dev = hx.setup(bp, degree=p, dims=dims, deform=deform)
+    host = hx.setup(bp, degree=p, dims=dims, deform=deform, host_setup=True)
+    assert np.array_equal(dev.coords, ref.coords)
+    assert np.array_equal(dev.diagonal(), ref.diagonal())
+    assert np.array_equal(host.exact, ref.exact)
+    if deform == "none":
+        assert np.array_equal(dev.exact, ref.exact)
+    else:
+        ulp = np.spacing(np.maximum(np.abs(ref.exact), 1e-300))
+        assert np.max(np.abs(dev.exact - ref.exact) / ulp) <= 2
+    for pr in (dev, host):
+        assert oracle.rel_max_diff(ref.rhs, pr.rhs) <= 1e-15
+    assert dev.setup_seconds > 0
