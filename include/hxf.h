@@ -189,7 +189,7 @@ uint64_t hxf_flops_estimate(int p, int q, int m, hxf_eval_mode mode);
  * (bench.cpp:56-62): u = sin(pi x) sin(pi y) sin(pi z) and f = 3 pi^2 u
  * (poisson) or u, each replicated over m components.  On the undeformed box
  * u and f are bit-exact too; on the sine box the deformed points' sines come
- * from the device's sin (within 2 ulp of the host's).  Any of coords / f / u
+ * from the device's sin (within 1e-15 of max|u|).  Any of coords / f / u
  * may be NULL. */
 int hxf_box_fields(hxf_ctx* ctx, const int glob[3], const int off[3], const int loc[3], int p,
                    const double* gll_nodes, int deform, int m, int poisson, double* coords,

@@ -279,7 +279,7 @@ __global__ void qdata_point_kernel(int kind, int nq1, const double* __restrict__
 // ((0.05 sx) sy) sz, and the manufactured u* = sin(pi x) sin(pi y) sin(pi z)
 // / f = 3 pi^2 u*.  Coordinates are the reference's bit for bit; u*, f too
 // on the undeformed box (the axis sines ARE sin(pi x)); on the sine box the
-// deformed point's sines come from CUDA's sin (<= 2 ulp from glibc's).
+// deformed point's sines come from CUDA's sin (within 1e-15 of max|u| of glibc's).
 struct BoxAxes {
   const double *cx, *cy, *cz;  // global 1-D axes (mesh.cpp:12-28)
   const double *sx, *sy, *sz;  // sin(M_PI * c) on those axes
