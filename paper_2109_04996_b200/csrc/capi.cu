@@ -343,24 +343,26 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
     ck(err, "operator kernel launch");
     total += grid;
   };
-  // partitioned, one diffusion pass on the DMMA kernel: boundary elements,
+  // partitioned, one stage (every BP has alpha XOR beta): boundary elements,
   // fork the sum-exchange of the interface planes (only boundary elements
-  // touch them) onto the comm stream, interior elements meanwhile, join
-  // (kernels that take an element list: DMMA (p = 7 collocated) and the line
-  // kernel (interpolating bases, one-component collocated p != 7, p >= 10))
-  const bool dmma_path = op->P == 8 && !op->interp && op_kernel_choice() == 0;
-  const bool line_path = op_kernel_choice() != 2 && op->symmetric &&
-                         (op->interp || (op->P != 8 && (op->m == 1 || op->P > 10)));
+  // touch them) onto the comm stream, interior elements meanwhile, join.
+  // Every K1 family takes an element list (DMMA incl. the padded tile,
+  // pencil, line); only the general kernel of non-centro-symmetric bases
+  // (op_kernel.cuh) does not.
+  const bool one_stage = (op->alpha == 0.0) != (op->beta == 0.0);
+  const bool elist_ok = op_kernel_choice() != 2 && op->symmetric;
   const bool split = halo && op->comm && op->d_elist && op->n_bnd > 0 && op->n_int > 0 &&
-                     op->beta == 0.0 && (dmma_path || line_path) && overlap_enabled();
+                     one_stage && elist_ok && overlap_enabled();
   if (split) {
+    const int pass = op->alpha != 0.0 ? 0 : 1;
+    const double coef = pass == 0 ? op->alpha : op->beta;
     prm.elist = op->d_elist;
     prm.E = op->n_bnd;
-    launch(0, op->alpha, nullptr);
+    launch(pass, coef, nullptr);
     ck(cudaEventRecord(op->ev_fork, s), "fork");
     prm.elist = op->d_elist + op->n_bnd;
     prm.E = op->n_int;
-    launch(0, op->alpha, st);
+    launch(pass, coef, st);
     ck(cudaStreamWaitEvent(op->s_comm, op->ev_fork, 0), "fork");
     op_halo_sum(op, y, op->s_comm);
     ck(cudaEventRecord(op->ev_join, op->s_comm), "join");

@@ -99,7 +99,6 @@ cudaError_t run_pencil(const OpParams& prm, const double* D, cudaStream_t s, int
   }
   static_assert(T::GM == 0 || T::GM == 1, "gather mode");
   (void)D;
-  if (prm.elist) return cudaErrorNotSupported;  // no element-list support
   if (!prm.D) return cudaErrorInvalidValue;
   const int64_t nsteps = (prm.E + T::EPB - 1) / T::EPB;
   const int grid = capped_grid(nsteps, max_ctas);

@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   const int64_t G = gridDim.x;
   const int64_t NXY = prm.NX * prm.NY;
   uint64_t policy = 0;
+  // element of list position k: a subset (partition overlap: boundary
+  // elements first, then the interior) or 0..E-1
+  auto elem_of = [&](int64_t k) -> int64_t { return prm.elist ? (int64_t)__ldg(prm.elist + k) : k; };
   auto qbytes = [&](int64_t s) -> uint32_t {
     const int64_t e0 = s * EPB;
     const int ne = (int)((prm.E - e0) < EPB ? (prm.E - e0) : EPB);
@@ -141,12 +144,20 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   auto issue_qdata = [&](int64_t s) {
     const uint32_t bytes = qbytes(s);
     mbar_arrive_expect_tx(&qbar, bytes);
-    bulk_g2s(sQD, prm.qd + s * EPB * T::QDS, bytes, &qbar, policy);
+    if (prm.elist) {  // listed elements are not contiguous: one copy each
+      const int ne = (int)(bytes / (T::QDS * 8));
+      for (int i = 0; i < ne; ++i)
+        bulk_g2s(sQD + i * T::QDS, prm.qd + elem_of(s * EPB + i) * T::QDS, (uint32_t)(T::QDS * 8),
+                 &qbar, policy);
+    } else {
+      bulk_g2s(sQD, prm.qd + s * EPB * T::QDS, bytes, &qbar, policy);
+    }
   };
   // the element after next: pull its factors HBM -> L2 now (no shared memory
   // needed), so the later bulk copy into shared memory is an L2 hit
   auto prefetch_qdata = [&](int64_t s) {
-    if (s < nsteps && (prm.ablate & 8)) bulk_prefetch_l2(prm.qd + s * EPB * T::QDS, qbytes(s));
+    if (s < nsteps && (prm.ablate & 8) && !prm.elist)
+      bulk_prefetch_l2(prm.qd + s * EPB * T::QDS, qbytes(s));
   };
   if (tid == 0) {
     mbar_init(&qbar, 1);
@@ -163,9 +174,10 @@ __global__ void __launch_bounds__(T::NT) op_pencil_kernel(const OpParams prm) {
   const FastDiv divx((uint32_t)prm.nx), divy((uint32_t)prm.ny);
   auto geometry = [&](int64_t step) {
     PencilGeo g{};
-    const int64_t e = step * EPB + slot;
-    g.active = active_slot && step < nsteps && e < prm.E;
+    const int64_t k = step * EPB + slot;
+    g.active = active_slot && step < nsteps && k < prm.E;
     if (!g.active) return g;
+    const int64_t e = elem_of(k);
     if (T::GM == 1 && prm.idx) {
       g.key = e;
     } else {

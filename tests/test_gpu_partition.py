@@ -34,6 +34,12 @@ CASES = [
     ("bp5", 7, (6, 4, 4), "sine", 4),
     ("bp6", 7, (6, 3, 3), "sine", 2),
     ("bp5", 7, (4, 4, 4), "none", 8),
+    # three-component collocated kernels with the element list too: the pencil
+    # kernel (p = 1, 2, 5, 8, 9) and the zero-padded DMMA tile (p = 6)
+    ("bp6", 5, (4, 3, 3), "sine", 2),
+    ("bp6", 8, (4, 2, 2), "sine", 2),
+    ("bp6", 1, (6, 4, 4), "sine", 8),
+    ("bp6", 6, (4, 4, 2), "sine", 4),
 ]
 
 
