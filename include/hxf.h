@@ -258,6 +258,22 @@ int hxf_comm_wrap_nccl(hxf_ctx* ctx, void* nccl_comm, hxf_comm** out);
 int hxf_comm_group_create(int nranks, hxf_comm_group** out);
 int hxf_comm_group_destroy(hxf_comm_group* group);
 int hxf_comm_create_group(hxf_ctx* ctx, hxf_comm_group* group, int rank, hxf_comm** out);
+/* Peer-to-peer communicator: every rank stores its interface planes and dot
+ * partials straight into the peers' mailboxes (NVLink peer stores between
+ * GPUs, plain stores on one GPU) with system-scope flags; kernels only, so
+ * CUDA-graph capturable.  Each rank allocates its mailbox (cap doubles per
+ * interface plane, >= the largest m * plane) with hxf_comm_p2p_alloc, which
+ * also returns its CUDA IPC handle; the caller gathers the handles (e.g. over
+ * torch.distributed) and every rank then creates the communicator from the
+ * nranks handles — or, for ranks of one process, from the nranks mailbox
+ * pointers (bases; NULL entries are opened from handles). */
+#define HXF_COMM_IPC_HANDLE_BYTES 64
+int hxf_comm_p2p_alloc(hxf_ctx* ctx, int nranks, int64_t cap, void** base,
+                       unsigned char handle[HXF_COMM_IPC_HANDLE_BYTES]);
+int hxf_comm_create_p2p(hxf_ctx* ctx, int nranks, int rank, int64_t cap, void* const* bases,
+                        const unsigned char* handles, hxf_comm** out);
+/* Free a mailbox from hxf_comm_p2p_alloc (after every communicator using it is destroyed). */
+int hxf_comm_p2p_free(hxf_ctx* ctx, void* base);
 int hxf_comm_destroy(hxf_comm* comm);
 int hxf_comm_rank(const hxf_comm* comm);
 int hxf_comm_size(const hxf_comm* comm);

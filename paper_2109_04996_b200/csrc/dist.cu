@@ -198,6 +198,168 @@ struct GroupComm final : Comm {
   }
 };
 
+// ---- peer-to-peer (NVLink / same-device) mailboxes ---------------------------
+// Every rank owns one device allocation (exported by CUDA IPC between
+// processes, or shared directly inside one process):
+//   mail  [2][N][cap] f64   exchange slots, by parity and source rank
+//   ar    [2][N][8]   f64   all-reduce slots
+//   xflag [2][N]      u64   exchange arrival counters (+1 per put CTA)
+//   aflag [2][N]      u64   all-reduce arrival values
+//   state: sseq[N], rseq[N], sdone[N], rdone[N], aseq (u64, local only)
+// A put kernel stores a packed plane straight into the PEER's slot (remote
+// stores over NVLink; plain stores on one device), fences at system scope
+// and bumps the peer's counter; the matching get kernel spins on its own
+// counter and copies the slot out.  Sequence numbers live on the device, so
+// the kernels are CUDA-graph capturable, and every slot is double-buffered by
+// the pair's transfer parity: a put of transfer k+2 can only run after its
+// rank's get of k+1, which the peer posted after reading transfer k.
+constexpr int kP2pMax = 16;
+constexpr int kP2pBlocks = 32;
+
+struct P2pLayout {
+  int N;
+  int64_t cap;
+  __host__ __device__ size_t mail_off() const { return 0; }
+  __host__ __device__ size_t ar_off() const { return size_t(2) * N * size_t(cap) * 8; }
+  __host__ __device__ size_t xflag_off() const { return ar_off() + size_t(2) * N * 8 * 8; }
+  __host__ __device__ size_t aflag_off() const { return xflag_off() + size_t(2) * N * 8; }
+  __host__ __device__ size_t state_off() const { return aflag_off() + size_t(2) * N * 8; }
+  __host__ __device__ size_t bytes() const { return state_off() + size_t(4 * N + 1) * 8; }
+};
+
+struct P2pPeers {
+  char* base[kP2pMax];
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// spin (bounded: a lost peer traps instead of hanging the GPU)
+__device__ __forceinline__ void wait_at_least(const unsigned long long* p, unsigned long long v) {
+  long long spins = 0;
+  while (ld_acquire_sys(p) < v) {
+    __nanosleep(64);
+    if (++spins > (1ll << 26)) __trap();
+  }
+}
+
+__global__ void p2p_put_kernel(P2pPeers pe, P2pLayout L, int rank, int peer, const double* __restrict__ send,
+                               int64_t n) {
+  char* mine = pe.base[rank];
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(mine + L.state_off());
+  const unsigned long long k = st[peer];  // sseq[peer]: updated only by the last CTA
+  const int par = int(k & 1);
+  double* dst = reinterpret_cast<double*>(pe.base[peer] + L.mail_off()) +
+                (size_t(par) * L.N + rank) * size_t(L.cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = send[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned long long* flag = reinterpret_cast<unsigned long long*>(pe.base[peer] + L.xflag_off()) +
+                               par * L.N + rank;
+    atomicAdd_system(flag, 1ull);
+    if (atomicAdd(&st[2 * L.N + peer], 1ull) == gridDim.x - 1) {  // sdone: last CTA
+      st[2 * L.N + peer] = 0;
+      st[peer] = k + 1;
+    }
+  }
+}
+
+__global__ void p2p_get_kernel(P2pPeers pe, P2pLayout L, int rank, int peer, double* __restrict__ recv,
+                               int64_t n) {
+  char* mine = pe.base[rank];
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(mine + L.state_off());
+  const unsigned long long j = st[L.N + peer];  // rseq[peer]
+  const int par = int(j & 1);
+  const unsigned long long* flag =
+      reinterpret_cast<const unsigned long long*>(mine + L.xflag_off()) + par * L.N + peer;
+  const unsigned long long target = (unsigned long long)kP2pBlocks * ((j >> 1) + 1);
+  if (threadIdx.x == 0) wait_at_least(flag, target);
+  __syncthreads();
+  (void)ld_acquire_sys(flag);  // every thread acquires the peer's stores
+  const double* src = reinterpret_cast<const double*>(mine + L.mail_off()) +
+                      (size_t(par) * L.N + peer) * size_t(L.cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    recv[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&st[3 * L.N + peer], 1ull) == gridDim.x - 1) {  // rdone
+    st[3 * L.N + peer] = 0;
+    st[L.N + peer] = j + 1;
+  }
+}
+
+// one CTA: put this rank's n (<= 8) values into every rank's slot, wait for
+// all N, sum in rank order (identical bits on every rank)
+__global__ void p2p_allreduce_kernel(P2pPeers pe, P2pLayout L, int rank, double* v, int n) {
+  char* mine = pe.base[rank];
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(mine + L.state_off());
+  const unsigned long long a = st[4 * L.N];
+  const int par = int(a & 1);
+  const unsigned long long val = (a >> 1) + 1;
+  const int t = threadIdx.x;
+  for (int i = t; i < L.N * n; i += blockDim.x) {
+    const int q = i / n, c = i - q * n;
+    reinterpret_cast<double*>(pe.base[q] + L.ar_off())[(size_t(par) * L.N + rank) * 8 + c] = v[c];
+  }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence_system();
+    for (int q = 0; q < L.N; ++q)
+      atomicExch_system(reinterpret_cast<unsigned long long*>(pe.base[q] + L.aflag_off()) + par * L.N + rank,
+                        val);
+    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(mine + L.aflag_off()) + par * L.N;
+    for (int q = 0; q < L.N; ++q) wait_at_least(fl + q, val);
+  }
+  __syncthreads();
+  (void)ld_acquire_sys(reinterpret_cast<const unsigned long long*>(mine + L.aflag_off()) + par * L.N);
+  if (t < n) {
+    const double* slots = reinterpret_cast<const double*>(mine + L.ar_off()) + size_t(par) * L.N * 8;
+    double s = 0.0;
+    for (int q = 0; q < L.N; ++q) s += slots[q * 8 + t];
+    v[t] = s;
+  }
+  __syncthreads();
+  if (t == 0) st[4 * L.N] = a + 1;
+}
+
+struct P2pComm final : Comm {
+  P2pLayout L{};
+  P2pPeers pe{};
+  void* local = nullptr;       // this rank's allocation (owned when allocated here)
+  bool owns_local = false;
+  std::vector<void*> opened;   // IPC-opened peer allocations
+  ~P2pComm() override {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    if (owns_local && local) cudaFree(local);
+  }
+  void allreduce_sum(double* dev, size_t n, cudaStream_t s) override {
+    for (size_t off = 0; off < n; off += 8) {
+      const int k = int(std::min<size_t>(8, n - off));
+      p2p_allreduce_kernel<<<1, 64, 0, s>>>(pe, L, rank, dev + off, k);
+      count_launch(1);
+      ck(cudaGetLastError(), "p2p allreduce");
+    }
+  }
+  void exchange(const std::vector<Xfer>& xs, cudaStream_t s) override {
+    for (const Xfer& x : xs) {
+      if (x.peer < 0 || x.peer >= size || x.peer == rank) fail(HXF_EINVAL, "p2p exchange: bad peer");
+      if (int64_t(x.n) > L.cap) fail(HXF_EINVAL, "p2p exchange: plane larger than the mailbox");
+      p2p_put_kernel<<<kP2pBlocks, 256, 0, s>>>(pe, L, rank, x.peer, x.send, int64_t(x.n));
+      count_launch(1);
+      ck(cudaGetLastError(), "p2p put");
+    }
+    for (const Xfer& x : xs) {
+      p2p_get_kernel<<<kP2pBlocks, 256, 0, s>>>(pe, L, rank, x.peer, x.recv, int64_t(x.n));
+      count_launch(1);
+      ck(cudaGetLastError(), "p2p get");
+    }
+  }
+};
+
 // ---- plane kernels -----------------------------------------------------------
 struct Plane {
   int axis;
@@ -417,6 +579,69 @@ int hxf_comm_create_group(hxf_ctx* ctx, hxf_comm_group* group, int rank, hxf_com
     h->impl = std::move(c);
     h->ctx = ctx;
     *out = h;
+  });
+}
+
+int hxf_comm_p2p_alloc(hxf_ctx* ctx, int nranks, int64_t cap, void** base,
+                       unsigned char handle[HXF_COMM_IPC_HANDLE_BYTES]) {
+  return guarded_dist([&] {
+    if (!ctx || !base) fail(HXF_EINVAL, "hxf_comm_p2p_alloc: NULL argument");
+    if (nranks < 1 || nranks > kP2pMax || cap < 1) fail(HXF_EINVAL, "hxf_comm_p2p_alloc: bad size");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const P2pLayout L{nranks, cap};
+    void* p = nullptr;
+    ck(cudaMalloc(&p, L.bytes()), "p2p mailbox");
+    ck(cudaMemset(p, 0, L.bytes()), "p2p mailbox");
+    ck(cudaDeviceSynchronize(), "p2p mailbox");
+    if (handle) {
+      cudaIpcMemHandle_t h{};
+      ck(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+      std::memcpy(handle, &h, sizeof h);
+    }
+    *base = p;
+  });
+}
+
+int hxf_comm_create_p2p(hxf_ctx* ctx, int nranks, int rank, int64_t cap, void* const* bases,
+                        const unsigned char* handles, hxf_comm** out) {
+  return guarded_dist([&] {
+    if (!ctx || !out || (!bases && !handles)) fail(HXF_EINVAL, "hxf_comm_create_p2p: NULL argument");
+    if (nranks < 1 || nranks > kP2pMax || rank < 0 || rank >= nranks || cap < 1)
+      fail(HXF_EINVAL, "hxf_comm_create_p2p: bad rank / size");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    auto c = std::make_unique<P2pComm>();
+    c->L = P2pLayout{nranks, cap};
+    c->rank = rank;
+    c->size = nranks;
+    c->graph_safe = true;
+    for (int q = 0; q < nranks; ++q) {
+      if (bases && bases[q]) {  // same process: direct pointers
+        c->pe.base[q] = static_cast<char*>(bases[q]);
+        continue;
+      }
+      if (!handles) fail(HXF_EINVAL, "hxf_comm_create_p2p: rank without a mailbox");
+      cudaIpcMemHandle_t h{};
+      std::memcpy(&h, handles + size_t(q) * HXF_COMM_IPC_HANDLE_BYTES, sizeof h);
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      c->opened.push_back(p);
+      c->pe.base[q] = static_cast<char*>(p);
+    }
+    if (!c->pe.base[rank]) fail(HXF_EINVAL, "hxf_comm_create_p2p: own mailbox missing");
+    auto* h = new hxf_comm();
+    h->impl = std::move(c);
+    h->ctx = ctx;
+    *out = h;
+  });
+}
+
+int hxf_comm_p2p_free(hxf_ctx* ctx, void* base) {
+  return guarded_dist([&] {
+    if (!ctx) fail(HXF_EINVAL, "hxf_comm_p2p_free: NULL context");
+    if (base) {
+      ck(cudaDeviceSynchronize(), "p2p mailbox");
+      ck(cudaFree(base), "p2p mailbox");
+    }
   });
 }
 

@@ -386,8 +386,70 @@ std::vector<std::shared_ptr<Communicator>> Communicator::group(const std::vector
   }
   return out;
 }
+std::vector<std::shared_ptr<Communicator>> Communicator::p2p_group(const std::vector<int>& devices,
+                                                                   int64_t cap) {
+  const int n = int(devices.size());
+  std::vector<std::shared_ptr<Device>> devs;
+  std::vector<std::shared_ptr<void>> boxes;
+  std::vector<void*> bases;
+  for (int r = 0; r < n; ++r) {
+    devs.push_back(std::make_shared<Device>(devices[size_t(r)]));
+    void* b = nullptr;
+    check(hxf_comm_p2p_alloc(devs.back()->ctx(), n, cap, &b, nullptr));
+    auto dev = devs.back();
+    boxes.emplace_back(b, [dev](void* p) { hxf_comm_p2p_free(dev->ctx(), p); });
+    bases.push_back(b);
+  }
+  std::vector<std::shared_ptr<Communicator>> out;
+  for (int r = 0; r < n; ++r) {
+    std::shared_ptr<Communicator> c(new Communicator());
+    c->dev_ = devs[size_t(r)];
+    c->mailbox_ = boxes[size_t(r)];
+    check(hxf_comm_create_p2p(c->dev_->ctx(), n, r, cap, bases.data(), nullptr, &c->comm_));
+    out.push_back(c);
+  }
+  // every rank's communicator reaches every mailbox: keep them all alive
+  for (auto& c : out) {
+    auto all = boxes;
+    c->group_ = nullptr;
+    c->mailbox_ = std::shared_ptr<void>(new std::vector<std::shared_ptr<void>>(all),
+                                        [](void* p) { delete static_cast<std::vector<std::shared_ptr<void>>*>(p); });
+  }
+  return out;
+}
+
+Communicator::P2pMailbox Communicator::alloc_p2p(int device, int nranks, int64_t cap) {
+  P2pMailbox m;
+  m.dev = Device::get(device);
+  m.handle.assign(HXF_COMM_IPC_HANDLE_BYTES, '\0');
+  check(hxf_comm_p2p_alloc(m.dev->ctx(), nranks, cap, &m.base,
+                           reinterpret_cast<unsigned char*>(m.handle.data())));
+  return m;
+}
+
+std::shared_ptr<Communicator> Communicator::p2p(const P2pMailbox& mine, int nranks, int rank,
+                                                int64_t cap, const std::vector<std::string>& handles) {
+  if (int(handles.size()) != nranks) throw std::invalid_argument("p2p: one handle per rank");
+  std::string all;
+  for (const auto& hd : handles) {
+    if (hd.size() != HXF_COMM_IPC_HANDLE_BYTES) throw std::invalid_argument("p2p: bad handle");
+    all += hd;
+  }
+  std::vector<void*> bases(size_t(nranks), nullptr);
+  bases[size_t(rank)] = mine.base;
+  std::shared_ptr<Communicator> c(new Communicator());
+  c->dev_ = mine.dev;
+  auto dev = mine.dev;
+  c->mailbox_ = std::shared_ptr<void>(mine.base, [dev](void* p) { hxf_comm_p2p_free(dev->ctx(), p); });
+  check(hxf_comm_create_p2p(c->dev_->ctx(), nranks, rank, cap, bases.data(),
+                            reinterpret_cast<const unsigned char*>(all.data()), &c->comm_));
+  return c;
+}
+
 Communicator::~Communicator() {
   if (comm_) hxf_comm_destroy(comm_);
+  comm_ = nullptr;
+  mailbox_.reset();  // after the communicator that used it
 }
 double Communicator::allreduce_sum(double v) const {
   DeviceBuffer b(dev_, 1);

@@ -105,6 +105,19 @@ class Communicator {
   static std::string unique_id();  // HXF_COMM_ID_BYTES bytes (rank 0 makes it)
   static std::shared_ptr<Communicator> nccl(int device, int nranks, int rank, const std::string& id);
   static std::vector<std::shared_ptr<Communicator>> group(const std::vector<int>& devices);
+  // peer-to-peer mailboxes (hxf_comm_create_p2p): ranks of this process
+  // (one context each) sharing pointers, or one rank per process: alloc_p2p
+  // returns this rank's IPC handle, p2p() opens the gathered handles
+  static std::vector<std::shared_ptr<Communicator>> p2p_group(const std::vector<int>& devices,
+                                                              int64_t cap);
+  struct P2pMailbox {
+    std::shared_ptr<Device> dev;
+    void* base = nullptr;
+    std::string handle;  // HXF_COMM_IPC_HANDLE_BYTES
+  };
+  static P2pMailbox alloc_p2p(int device, int nranks, int64_t cap);
+  static std::shared_ptr<Communicator> p2p(const P2pMailbox& mine, int nranks, int rank, int64_t cap,
+                                           const std::vector<std::string>& handles);
   ~Communicator();
   Communicator(const Communicator&) = delete;
   Communicator& operator=(const Communicator&) = delete;
@@ -118,6 +131,7 @@ class Communicator {
   Communicator() = default;
   std::shared_ptr<Device> dev_;
   std::shared_ptr<hxf_comm_group> group_;
+  std::shared_ptr<void> mailbox_;  // p2p: the mailbox this rank owns (freed after the comm)
   hxf_comm* comm_ = nullptr;
 };
 

@@ -43,6 +43,27 @@ def nccl_communicator(device: int) -> "_core.Communicator":
     return _core.Communicator.nccl(device, dist.get_world_size(), dist.get_rank(), uid)
 
 
+def p2p_capacity(dims_local, p: int, m: int) -> int:
+    """Doubles per mailbox slot: the largest interface plane of a sub-box of
+    dims_local elements, times the components."""
+    nx, ny, nz = (int(d) * p + 1 for d in dims_local)
+    return m * max(ny * nz, nx * nz, nx * ny)
+
+
+def p2p_communicator(device: int, cap: int) -> "_core.Communicator":
+    """Peer-to-peer hxf communicator of this rank (one process per GPU,
+    torch.distributed initialised): allocate the mailbox, all-gather the CUDA
+    IPC handles, open the peers'.  The solver then exchanges planes by direct
+    peer stores (NVLink) and reduces dots in peer memory, graph-captured."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    mailbox, handle = _core.Communicator.p2p_alloc(device, world, cap)
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(handle))
+    return _core.Communicator.p2p(mailbox, world, rank, cap, handles)
+
+
 def partition_summary(dims, nranks: int, p: int) -> dict:
     """Process grid, per-rank sub-box sizes and the largest interface plane."""
     subs = [_core.subdomain(tuple(dims), nranks, r) for r in range(nranks)]

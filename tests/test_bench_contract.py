@@ -70,3 +70,12 @@ def test_our_arm_verifies_its_timed_result():
     assert v["iterations"] == [20, 20]
     assert r["cpu_baseline"]["value"] > 0 and r["cpu_baseline"]["cores"] >= 1
     assert r["e2e"]["serial"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_group_emulation_runs_the_partitioned_path():
+    """bench.py --group 2: the --gpus N code path (partition, exchange,
+    all-reduce) on one GPU, checked against the single-domain solve."""
+    r = run_bench("--group", "2", "--steps", "2", "--warmup", "1", "--elems", "4")
+    assert r["emulated_ranks"] == 2 and r["value"] > 0
+    assert r["verification"]["ok"], r["verification"]
