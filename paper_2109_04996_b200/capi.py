@@ -34,7 +34,7 @@ EXPORTS = (
     "hxf_elem_restriction_is_structured", "hxf_elem_restriction_apply",
     "hxf_elem_restriction_multiplicity", "hxf_elem_restriction_gather_scalar",
     "hxf_contract_batch", "hxf_apply_tensor_3d", "hxf_flops_estimate", "hxf_box_fields",
-    "hxf_operator_set_constrained",
+    "hxf_operator_set_constrained", "hxf_comm_p2p_alloc", "hxf_comm_create_p2p", "hxf_comm_p2p_free",
 )
 
 
@@ -137,6 +137,9 @@ def lib() -> C.CDLL:
     L.hxf_apply_tensor_3d.argtypes = [P, I, I, P, P, I, I, I, P, I64, P, I64, I]
     L.hxf_box_fields.argtypes = [P, P, P, P, I, P, I, I, I, P, P, P, I]
     L.hxf_operator_set_constrained.argtypes = [P, P, D, I]
+    L.hxf_comm_p2p_alloc.argtypes = [P, I, I64, C.POINTER(P), P]
+    L.hxf_comm_create_p2p.argtypes = [P, I, I, I64, P, P, C.POINTER(P)]
+    L.hxf_comm_p2p_free.argtypes = [P, P]
     L.hxf_flops_estimate.restype = C.c_uint64
     L.hxf_flops_estimate.argtypes = [I, I, I, I]
     _lib = L
