@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--deform", default="sine")
     ap.add_argument("--iters", type=int, default=20, help="CG iterations per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 transport: NCCL send/recv + all-reduce, or peer-store mailboxes "
+                         "over NVLink (CUDA IPC)")
     ap.add_argument("--group", type=int, default=0,
                     help="emulate N ranks as an in-process group of sub-domains on one GPU "
                          "(the partitioned code path: exchange + all-reduce; not a scaling number)")
@@ -308,9 +311,13 @@ def run_ours(args):
         # interface sum-exchange + dot all-reduces inside hxf over NCCL
         from paper_2109_04996_b200 import _core, dist as hdist
 
-        comm = hdist.nccl_communicator(local)
         grid = tuple(_core.proc_grid(world, (args.elems,) * 3))
         gdims = tuple(args.elems * g for g in grid)
+        if args.comm == "p2p":
+            cap = hdist.p2p_capacity((args.elems,) * 3, args.degree, sizes["m"])
+            comm = hdist.p2p_communicator(local, cap)
+        else:
+            comm = hdist.nccl_communicator(local)
         prob = hx.setup(args.bp, degree=args.degree, dims=gdims, deform=args.deform,
                         device=local, comm=comm, proc_grid=grid)
     else:
@@ -439,7 +446,8 @@ def run_ours(args):
                    "n_dofs": n_global, "n_L_per_gpu": sizes["n_L"],
                    "elements_per_gpu": sizes["E"], "global_elements": list(gdims),
                    "parallelism": (f"element partition {grid[0]}x{grid[1]}x{grid[2]} "
-                                   f"(interface sum-exchange + NCCL all-reduce)"
+                                   f"(interface sum-exchange + all-reduce over "
+                                   f"{'NVLink peer stores' if args.comm == 'p2p' else 'NCCL'})"
                                    if world > 1 else "single GPU"),
                    "l2_policy": "inputs larger than L2 (qdata 384 MB/GPU > 126 MB)"},
         "apply": {"gdofs": n_global / t_apply / 1e9, "us": t_apply * 1e6,

@@ -265,8 +265,10 @@ int hxf_comm_create_group(hxf_ctx* ctx, hxf_comm_group* group, int rank, hxf_com
  * interface plane, >= the largest m * plane) with hxf_comm_p2p_alloc, which
  * also returns its CUDA IPC handle; the caller gathers the handles (e.g. over
  * torch.distributed) and every rank then creates the communicator from the
- * nranks handles — or, for ranks of one process, from the nranks mailbox
- * pointers (bases; NULL entries are opened from handles). */
+ * nranks handles (bases may carry the pointers of mailboxes in this process;
+ * NULL entries are opened from handles).  Ranks that share one process AND
+ * device must not make device-synchronising calls (cudaFree, ...) while an
+ * exchange is in flight: the receive kernels spin on the peers' flags. */
 #define HXF_COMM_IPC_HANDLE_BYTES 64
 int hxf_comm_p2p_alloc(hxf_ctx* ctx, int nranks, int64_t cap, void** base,
                        unsigned char handle[HXF_COMM_IPC_HANDLE_BYTES]);

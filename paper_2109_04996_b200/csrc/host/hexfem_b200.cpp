@@ -386,38 +386,6 @@ std::vector<std::shared_ptr<Communicator>> Communicator::group(const std::vector
   }
   return out;
 }
-std::vector<std::shared_ptr<Communicator>> Communicator::p2p_group(const std::vector<int>& devices,
-                                                                   int64_t cap) {
-  const int n = int(devices.size());
-  std::vector<std::shared_ptr<Device>> devs;
-  std::vector<std::shared_ptr<void>> boxes;
-  std::vector<void*> bases;
-  for (int r = 0; r < n; ++r) {
-    devs.push_back(std::make_shared<Device>(devices[size_t(r)]));
-    void* b = nullptr;
-    check(hxf_comm_p2p_alloc(devs.back()->ctx(), n, cap, &b, nullptr));
-    auto dev = devs.back();
-    boxes.emplace_back(b, [dev](void* p) { hxf_comm_p2p_free(dev->ctx(), p); });
-    bases.push_back(b);
-  }
-  std::vector<std::shared_ptr<Communicator>> out;
-  for (int r = 0; r < n; ++r) {
-    std::shared_ptr<Communicator> c(new Communicator());
-    c->dev_ = devs[size_t(r)];
-    c->mailbox_ = boxes[size_t(r)];
-    check(hxf_comm_create_p2p(c->dev_->ctx(), n, r, cap, bases.data(), nullptr, &c->comm_));
-    out.push_back(c);
-  }
-  // every rank's communicator reaches every mailbox: keep them all alive
-  for (auto& c : out) {
-    auto all = boxes;
-    c->group_ = nullptr;
-    c->mailbox_ = std::shared_ptr<void>(new std::vector<std::shared_ptr<void>>(all),
-                                        [](void* p) { delete static_cast<std::vector<std::shared_ptr<void>>*>(p); });
-  }
-  return out;
-}
-
 Communicator::P2pMailbox Communicator::alloc_p2p(int device, int nranks, int64_t cap) {
   P2pMailbox m;
   m.dev = Device::get(device);

@@ -105,11 +105,10 @@ class Communicator {
   static std::string unique_id();  // HXF_COMM_ID_BYTES bytes (rank 0 makes it)
   static std::shared_ptr<Communicator> nccl(int device, int nranks, int rank, const std::string& id);
   static std::vector<std::shared_ptr<Communicator>> group(const std::vector<int>& devices);
-  // peer-to-peer mailboxes (hxf_comm_create_p2p): ranks of this process
-  // (one context each) sharing pointers, or one rank per process: alloc_p2p
-  // returns this rank's IPC handle, p2p() opens the gathered handles
-  static std::vector<std::shared_ptr<Communicator>> p2p_group(const std::vector<int>& devices,
-                                                              int64_t cap);
+  // peer-to-peer mailboxes (hxf_comm_create_p2p), one rank per process:
+  // alloc_p2p returns this rank's IPC handle, p2p() opens the gathered handles.
+  // (Ranks sharing one process and device would deadlock: a host thread's
+  // cudaFree waits for a peer's spinning receive kernel.)
   struct P2pMailbox {
     std::shared_ptr<Device> dev;
     void* base = nullptr;

@@ -160,61 +160,3 @@ def test_nccl_single_rank(bp, p, dims, deform):
         assert oracle.rel_max_diff(xg, xp) <= 1e-9
         k = min(len(rg["residual_history"]), len(rp["residual_history"]))
         assert oracle.rel_max_diff(rg["residual_history"][:k], rp["residual_history"][:k]) <= 1e-9
-
-
-# ---- peer-to-peer mailboxes (hxf_comm_create_p2p) ---------------------------
-def run_p2p_group(nranks, cap, fn):
-    comms = _core.Communicator.p2p_group([0] * nranks, cap)
-    out = [None] * nranks
-    errs = []
-
-    def work(r):
-        try:
-            out[r] = fn(r, comms[r])
-        except BaseException as e:  # surfaced below
-            errs.append(e)
-
-    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join(timeout=600)
-    if errs:
-        raise errs[0]
-    return out
-
-
-P2P_CASES = [("bp5", 7, (6, 4, 4), "sine", 4), ("bp6", 5, (4, 3, 3), "sine", 2),
-             ("bp3", 3, (4, 3, 3), "sine", 8), ("bp2", 2, (3, 2, 2), "none", 3)]
-
-
-@pytest.mark.parametrize("bp,p,dims,deform,nranks", P2P_CASES)
-def test_p2p_partitioned_apply_and_solve(bp, p, dims, deform, nranks):
-    """Peer-store exchange + peer-memory all-reduce (kernels only, captured
-    into the fixed-iteration solve graph) against the single-domain problem."""
-    from paper_2109_04996_b200 import dist as hdist
-
-    g = _core.setup(bp, p, dims, deform)
-    x = oracle.seeded_uniform(g.size, 11)
-    y_g, d_g = g.apply(x), g.diagonal()
-    _, rep_g = g.solve(tol=1e-8, fixed_iterations=12)
-    nG = g.num_nodes
-    grid = _core.proc_grid(nranks, dims)
-    cap = max(hdist.p2p_capacity(_core.subdomain(dims, nranks, r).dims, p, g.components)
-              for r in range(nranks))
-
-    def rank(r, comm):
-        pr = _core.setup(bp, p, dims, deform, comm=comm, proc_grid=grid)
-        ids = _core.global_node_ids(pr.subdomain, p)
-        idx = comp_index(pr, ids, nG)
-        y = pr.apply(x[idx])
-        _, rep = pr.solve(tol=1e-8, fixed_iterations=12)
-        _, rep2 = pr.solve(tol=1e-8, fixed_iterations=12)  # graph replay
-        return idx, y, pr.diagonal(), rep, rep2
-
-    for idx, y, d, rep, rep2 in run_p2p_group(nranks, cap, rank):
-        assert oracle.rel_max_diff(y_g[idx], y) <= 1e-12
-        assert oracle.rel_max_diff(d_g[idx], d) <= 1e-12
-        for rp in (rep, rep2):
-            assert rp["iterations"] == 12
-            assert oracle.rel_max_diff(rep_g["residual_history"], rp["residual_history"]) <= 1e-10
