@@ -7,6 +7,7 @@
 #include "op_pencil.cuh"
 #include "op_dmma.cuh"
 #include "op_line.cuh"
+#include "op_dmmaeo.cuh"
 
 namespace hxf {
 namespace {
@@ -138,6 +139,32 @@ cudaError_t run_dmma(const OpParams& prm, cudaStream_t s, int* grid_out) {
   return err;
 }
 
+// p = 8..15 collocated diffusion, even-odd halves on the FP64 tensor cores
+// (op_dmmaeo.cuh); structured box only (lattice gather).
+template <class T>
+cudaError_t run_dmmaeo(const OpParams& prm, cudaStream_t s, int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_dmmaeo_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  if (!prm.D || prm.idx || prm.cons_mode == 2) return cudaErrorInvalidValue;
+  const int grid = capped_grid(prm.E, max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  const cudaError_t err =
+      launch_pdl_if(pdl_enabled() || prm.pdl, kern, dim3(grid), dim3(T::NT), T::SMEM_BYTES, s, prm);
+  count_launch();
+  return err;
+}
+
 template <int NC, int NW, int NP = 8>
 cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
   if constexpr (NP == 8 && NW == 4) {
@@ -190,6 +217,14 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
     if (qk == 1 && op_kernel_choice() == 0) {
       if (NC == 1) return run_dmma_gm<1>(prm, s, g);
       if (NC == 3) return run_dmma_gm<3>(prm, s, g);
+    }
+  }
+  if constexpr (!INTERP && P >= 9 && P <= 16) {
+    // high orders: even-odd halves on the FP64 tensor cores (structured box)
+    if (qk == 1 && op_kernel_choice() == 0 && dmmaeo_enabled(P, NC) && !prm.idx &&
+        prm.cons_mode != 2 && centro_symmetric(P, Q, false, B, D)) {
+      if (NC == 1) return run_dmmaeo<EoTraits<P, 1>>(prm, s, g);
+      if (NC == 3) return run_dmmaeo<EoTraits<P, 3>>(prm, s, g);
     }
   }
   if constexpr (!INTERP && P == 7) {

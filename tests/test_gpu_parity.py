@@ -194,6 +194,27 @@ def test_apply_vs_oracle_across_orders(ctx, bp, p, dims):
     assert oracle.rel_max_diff(pr.apply(x), op.apply(x)) <= APPLY_TOL
 
 
+# even-odd FP64 tensor-core kernel (op_dmmaeo.cuh; dispatched for p >= 12 one
+# component, p >= 11 three): odd and even N = p+1, box-constrained sine
+# meshes; the lower orders of the list run the line / pencil kernels
+DMMAEO_CASES = [("bp5", 8, (2, 3, 2)), ("bp5", 9, (2, 2, 2)), ("bp5", 10, (2, 1, 2)),
+                ("bp5", 11, (1, 2, 2)), ("bp5", 12, (2, 1, 1)), ("bp5", 13, (1, 2, 1)),
+                ("bp5", 14, (1, 1, 2)), ("bp5", 15, (2, 1, 1)), ("bp6", 8, (2, 2, 1)),
+                ("bp6", 11, (1, 2, 2)), ("bp6", 12, (1, 1, 2)), ("bp6", 15, (1, 1, 1))]
+
+
+@pytest.mark.parametrize("bp,p,dims", DMMAEO_CASES)
+def test_apply_even_odd_tensor_core_orders(ctx, bp, p, dims):
+    pr = oracle.setup(bp, p, dims, "sine")
+    op = op_from_oracle(ctx, pr, indices=False)
+    x = oracle.seeded_uniform(pr.size, 7 + p)
+    y = op.apply(x)
+    assert oracle.rel_max_diff(pr.apply(x), y) <= APPLY_TOL
+    cons = pr.constrained
+    for c in range(pr.components):
+        assert np.array_equal(y[c * pr.num_nodes + cons], x[c * pr.num_nodes + cons])
+
+
 def test_device_memspace_and_fused_dot(ctx):
     import torch
     pr = oracle.setup("bp5", 7, (4, 4, 4), "sine")
@@ -228,6 +249,9 @@ KERNEL_FAMILIES = [
     ("bp1", 3, (5, 4, 3)),   # line, mass
     ("bp2", 4, (3, 3, 2)),   # line, mass, three components
     ("bp5", 1, (7, 6, 5)),   # line, 64-thread CTAs
+    ("bp5", 12, (2, 2, 2)),  # even-odd DMMA, odd N
+    ("bp5", 15, (2, 2, 1)),  # even-odd DMMA, even N
+    ("bp6", 11, (2, 1, 2)),  # even-odd DMMA, three components
 ]
 
 
