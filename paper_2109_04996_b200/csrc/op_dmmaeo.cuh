@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
   pdl_wait();  // x, y, stop and the PCG state come from the previous kernels
   if (prm.stop && *prm.stop) return;
 
+  const bool skipc = (prm.ablate & 16) != 0;  // measurement-only: no tensor-core products
   const int tid = threadIdx.x;
   const int w = tid >> 5, l = tid & 31, g = l >> 2, t = l & 3;
   double* SU = eo_smem;            // U, then V0, then x^T + y^T
@@ -135,8 +136,8 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
         const int a = 4 * ks + t;
         double e, f;
         evod(S[T::off(k, row, a)], S[T::off(k, row, N - 1 - a)], a, e, f);
-        dmma(pe0, pe1, e, me[ks]);
-        dmma(po0, po1, f, mo[ks]);
+        if (!skipc) dmma(pe0, pe1, e, me[ks]);
+        if (!skipc) dmma(po0, po1, f, mo[ks]);
       }
       out[mt * 4 + 0] = pe0 + po0;
       out[mt * 4 + 1] = pe1 + po1;
@@ -155,8 +156,8 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
         const int b = 4 * ks + t;
         double e, f;
         evod(X(b, cb), X(N - 1 - b, cb), b, e, f);
-        dmma(pe0, pe1, me[ks], e);
-        dmma(po0, po1, mo[ks], f);
+        if (!skipc) dmma(pe0, pe1, me[ks], e);
+        if (!skipc) dmma(po0, po1, mo[ks], f);
       }
       out[nt * 2 + 0] = pe0 + po0;
       out[nt * 2 + 1] = pe1 + po1;
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
     return q;
   };
   auto issue_gather = [&](const Geo& q, int c, double* dst) {
+    if (prm.ablate & 1) return;  // measurement-only: no gather traffic
     const double* src = prm.x + c * prm.n_L + q.base;
     for (int n = tid; n < N3; n += NT) {
       const int k = n / NN, rem = n - k * NN, j = rem / N, i = rem - j * N;
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
   for (; s < nsteps; s += G) {
     const bool has_next = s + G < nsteps;
     // factors of the next element: HBM -> L2 while this one computes
-    if (tid == 0 && has_next) bulk_prefetch_l2(prm.qd + elem(s + G) * T::QDS, (uint32_t)(T::QDS * 8));
+    if (tid == 0 && has_next && !(prm.ablate & 4)) bulk_prefetch_l2(prm.qd + elem(s + G) * T::QDS, (uint32_t)(T::QDS * 8));
     Geo nxt = cur;
     const double* qe = prm.qd + cur.e * T::QDS;
 #pragma unroll 1
@@ -319,7 +321,9 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
             const double* qp = qe + k * NN + R * N;
 #pragma unroll
             for (int m = 0; m < 6; ++m) {
-              if constexpr (!T::ODD) {  // (odd N: rows of the factor planes are not 16-byte aligned)
+              if (prm.ablate & 4) {  // measurement-only: no factor traffic
+                sv[m][0] = sv[m][1] = 1.0 + m;
+              } else if constexpr (!T::ODD) {  // (odd N: rows of the factor planes are not 16-byte aligned)
                 const double2 a = __ldg(reinterpret_cast<const double2*>(qp + m * N3 + (hp ? C3 : C0)));
                 sv[m][0] = a.x;
                 sv[m][1] = a.y;
