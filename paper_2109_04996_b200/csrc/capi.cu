@@ -516,13 +516,22 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
   device_apply(op, p, Ap, s, op->d_part, &nparts, &op->d_state->stop, /*zero_y=*/false,
                op->d_state, /*halo=*/true, serp & (odd ^ 1));
   if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time (single GPU: K1 alone)
+  const int xmode = !xb ? 0 : ((it & 1) ? 1 : 2);
+  double* pout = !xb ? pA : ((it & 1) ? pB : pA);
+  // single domain: update + direction as one cooperative kernel (grid barrier
+  // between them, z kept on chip) — no all-reduce has to sit in between
+  if (!op->comm && !op->d_own &&
+      pcg_step_fusable(op->n_L, ps.dinv, r, ps.dx, p, xmode == 2 ? pA : nullptr, pout, Ap)) {
+    ck(pcg_launch_step(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,
+                       xmode == 2 ? pA : nullptr, pout, Ap, op->d_mask, vpart, serp & odd, xmode),
+       "pcg step");
+    return;
+  }
   op_allreduce(op, red, 1, s);                     // pAp
   ck(pcg_launch_update(s, op->d_state, it, op->n_L, op->m, ps.dinv, r, Ap, op->d_own, vpart,
                        serp & odd),
      "pcg update");
   op_allreduce(op, red + 1, 2, s);  // r.r, r.z
-  const int xmode = !xb ? 0 : ((it & 1) ? 1 : 2);
-  double* pout = !xb ? pA : ((it & 1) ? pB : pA);
   ck(pcg_launch_direction(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,
                           xmode == 2 ? pA : nullptr, pout, Ap, op->d_mask, op->d_own, vpart,
                           serp & (odd ^ 1), xmode),

@@ -25,6 +25,7 @@ struct PcgState {
   int it, stop, converged, error, limit, fixed;
   int stop_update;  // iteration whose update kernel stopped the solve (pAp check), 0 = none
   unsigned int counter[4];  // last-block counters: K1, update, direction, init
+  unsigned int gbar[2];     // grid barrier of the fused update + direction kernel: count, generation
 };
 
 // Last-CTA finalisation of p.(A p) inside the operator kernel (PCG only):

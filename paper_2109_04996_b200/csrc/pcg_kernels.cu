@@ -21,6 +21,8 @@
 // run (the reference's dot_deterministic, parallel.cpp:69-106, plays that
 // role).  Scalars are read at kernel start and written only by the last CTA
 // (or, on an early stop, by CTA 0 — nothing reads them later in that kernel).
+#include <cstdlib>
+
 #include "pcg_device.cuh"
 #include "pcg_kernels.h"
 
@@ -360,6 +362,238 @@ __global__ void __launch_bounds__(VT, 4)
   }
 }
 
+// ---------------------------------------------------------------- fused step
+// Update and direction of iteration `it` in one persistent cooperative kernel
+// (single domain, one CTA per SM): phase 1 is the update kernel's
+// r -= alpha Ap with the r.r / r.z partials over grid-stride steps, z = r/d of
+// the CTA's first zcap pairs kept in shared memory; a grid barrier; every CTA
+// sums the partials in the same fixed order (same bits everywhere); phase 2
+// is the direction kernel over the same pairs in the opposite step order (the
+// windows phase 1 touched last, still in L2, first; then the cached z).
+// Saves the r and 1/d re-reads of the cached pairs (2/3 of the vectors at C3)
+// and one kernel boundary per iteration.
+constexpr int ST_NT = 1024;
+constexpr int ST_SMEM = 192 * 1024;
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = gen;
+    const unsigned int g0 = *vgen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*vgen == g0) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int ST_U>  // grid-stride steps per loop trip (loads of all of them first)
+__global__ void __launch_bounds__(ST_NT, 1)
+    pcg_step_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
+                    const double* __restrict__ d, double* __restrict__ r, double* __restrict__ x,
+                    const double* p, const double* pprev, double* pout, double* __restrict__ Ap,
+                    const uint32_t* cons_mask, double* part, int rev, int xmode) {
+  extern __shared__ double2 zc[];
+  __shared__ double scratch[ST_NT / 32];
+  constexpr int zcap = ST_SMEM / 16;
+  if (st->stop) return;  // stopped in an earlier iteration
+  const double pap = st->red[0];
+  const double rho = st->rho;
+  const int G = gridDim.x;
+  const int64_t h = n_L * m / 2;  // pairs (n_L even)
+  // grid-stride steps j: the CTA's pair of step j (phase-1 order; -1 past the
+  // end) — every step is one contiguous window of the vectors, so each phase
+  // sweeps them (serpentine L2 reuse with the operator kernels as before)
+  // (32-bit pair indices: the launcher requires h < 2^31)
+  const int hh = (int)h;
+  const int span = G * ST_NT;
+  const int nj = (hh + span - 1) / span;
+  auto pair_at = [&](int j) -> int {
+    const int k = (j * G + (int)blockIdx.x) * ST_NT + (int)threadIdx.x;
+    return k < hh ? (rev ? hh - 1 - k : k) : -1;
+  };
+  double2* x2 = reinterpret_cast<double2*>(x);
+  const double alpha_prev = xmode == 2 ? st->alpha_prev : 0.0;
+  // pcg.cpp:74-82 (as pcg_update_kernel) and, on a stop there, the pending
+  // batched x update (as pcg_direction_kernel's stopped branch)
+  if (!isfinite(pap) || pap <= 0.0) {
+    const bool err = !isfinite(pap) || rho != 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->pap = pap;
+      if (!isfinite(pap)) st->error = PCG_ERR_APPLY_NAN;
+      else if (rho == 0.0) st->converged = 1;
+      else st->error = PCG_ERR_INDEFINITE;
+      st->stop_update = it;
+      st->stop = 1;
+    }
+    if (xmode == 2 && !err) {
+      const double2* q2 = reinterpret_cast<const double2*>(pprev);
+      for (int j = 0; j < nj; ++j) {
+        const int k = pair_at(j);
+        if (k < 0) continue;
+        double2 xv = x2[k];
+        const double2 pv = q2[k];
+        xv.x = fma(alpha_prev, pv.x, xv.x);
+        xv.y = fma(alpha_prev, pv.y, xv.y);
+        x2[k] = xv;
+      }
+    }
+    return;
+  }
+  const double alpha = rho / pap;
+  const double2 one2 = make_double2(1.0, 1.0);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  const double2* d2 = reinterpret_cast<const double2*>(d);
+  double2* a2 = reinterpret_cast<double2*>(Ap);
+
+  // ---- phase 1: r -= alpha Ap; r.r, r.z (pcg.cpp:84-88) ----
+  // (ST_U steps per trip, loads first: enough bytes in flight at one CTA per SM)
+  double rr = 0.0, rz = 0.0;
+  for (int j0 = 0; j0 < nj; j0 += ST_U) {
+    int k[ST_U];
+    double2 rv[ST_U], av[ST_U], dv[ST_U];
+#pragma unroll
+    for (int u = 0; u < ST_U; ++u) {
+      k[u] = j0 + u < nj ? pair_at(j0 + u) : -1;
+      if (k[u] >= 0) {
+        rv[u] = r2[k[u]];
+        av[u] = a2[k[u]];
+        dv[u] = d ? d2[k[u]] : one2;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ST_U; ++u) {
+      if (k[u] < 0) continue;
+      double2 v = rv[u];
+      v.x -= alpha * av[u].x;
+      v.y -= alpha * av[u].y;
+      r2[k[u]] = v;
+      const double2 z = make_double2(v.x * dv[u].x, v.y * dv[u].y);
+      rr += v.x * v.x + v.y * v.y;
+      rz += v.x * z.x + v.y * z.y;
+      const int q = (j0 + u) * ST_NT + (int)threadIdx.x;
+      if (q < zcap) zc[q] = z;
+    }
+  }
+  {
+    const double s0 = block_sum<ST_NT>(rr, scratch);
+    const double s1 = block_sum<ST_NT>(rz, scratch);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = s0;
+      part[G + blockIdx.x] = s1;
+    }
+  }
+  grid_barrier(&st->gbar[0], &st->gbar[1]);
+  __shared__ double tot[2];
+  {
+    const double trr = pcg_sum_partials<ST_NT>(part, G, scratch);
+    const double trz = pcg_sum_partials<ST_NT>(part + G, G, scratch);
+    if (threadIdx.x == 0) {
+      tot[0] = trr;
+      tot[1] = trz;
+    }
+    __syncthreads();
+  }
+  const double trr = tot[0], trz = tot[1];
+
+  // ---- phase 2: convergence (pcg.cpp:90-99), x += alpha p, p = z + beta p,
+  //      Ap preset (as pcg_direction_kernel) ----
+  const double res = sqrt(trr);
+  const bool bad = !isfinite(res);
+  const bool conv = res <= st->target;
+  const bool stop = bad || (conv && !st->fixed) || it == st->limit || res == 0.0;
+  const double beta = trz / rho;
+  const bool xupd = xmode != 1 || stop;
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* pp2 = reinterpret_cast<const double2*>(xmode == 2 ? pprev : p);
+  double2* po2 = reinterpret_cast<double2*>(pout);
+  double cc = 0.0;
+  for (int j0 = nj - 1; j0 >= 0; j0 -= ST_U) {
+    int k[ST_U];
+    double2 pv[ST_U], xv[ST_U], qv[ST_U], z[ST_U];
+#pragma unroll
+    for (int u = 0; u < ST_U; ++u) {
+      const int j = j0 - u;
+      k[u] = j >= 0 ? pair_at(j) : -1;
+      if (k[u] < 0) continue;
+      pv[u] = p2[k[u]];
+      if (xupd) xv[u] = x2[k[u]];
+      if (xupd && xmode == 2) qv[u] = pp2[k[u]];
+      const int q = j * ST_NT + (int)threadIdx.x;
+      if (!stop) {
+        if (q < zcap) {
+          z[u] = zc[q];
+        } else {
+          const double2 rv = r2[k[u]], dv = d ? d2[k[u]] : one2;
+          z[u] = make_double2(rv.x * dv.x, rv.y * dv.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ST_U; ++u) {
+      if (k[u] < 0) continue;
+      if (xupd) {
+        double2 xn = xv[u];
+        if (xmode == 2) {
+          xn.x = fma(alpha_prev, qv[u].x, xn.x);
+          xn.y = fma(alpha_prev, qv[u].y, xn.y);
+        }
+        xn.x = fma(alpha, pv[u].x, xn.x);
+        xn.y = fma(alpha, pv[u].y, xn.y);
+        x2[k[u]] = xn;
+      }
+      if (stop) continue;
+      double2 pn;
+      pn.x = z[u].x + beta * pv[u].x;
+      pn.y = z[u].y + beta * pv[u].y;
+      po2[k[u]] = pn;
+      int64_t node = 2 * (int64_t)k[u];
+      if (m > 1) node -= (node / n_L) * n_L;
+      const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
+      a2[k[u]] = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
+      if (w & 1u) cc += pn.x * pn.x;
+      if (w & 2u) cc += pn.y * pn.y;
+    }
+  }
+  const double sc = block_sum<ST_NT>(cc, scratch);
+  if (threadIdx.x == 0) part[2 * G + blockIdx.x] = sc;
+  if (!pcg_last_cta(&st->counter[2])) return;
+  const double tc = pcg_sum_partials<ST_NT>(part + 2 * G, G, scratch);
+  if (threadIdx.x == 0) {
+    st->counter[2] = 0;
+    st->pap = pap;
+    st->alpha = alpha;
+    st->red[1] = trr;
+    st->red[2] = trz;
+    if (stop) {
+      if (bad) {
+        st->error = PCG_ERR_RESID;
+      } else {
+        st->it = it;
+        st->res = res;
+        hist[it] = res;
+        if (conv) st->converged = 1;
+      }
+      st->stop = 1;
+      return;
+    }
+    st->red[3] = tc;
+    st->it = it;
+    st->res = res;
+    hist[it] = res;
+    if (conv) st->converged = 1;
+    st->beta = beta;
+    st->rho = trz;
+    st->alpha_prev = alpha;
+  }
+}
+
 // y = x on constrained rows, 0 elsewhere: the RED target of an operator apply
 // (operator.cpp:87-90,141-143).  With an owner mask only the owner presets
 // (a following interface sum-exchange then leaves exactly x).
@@ -425,6 +659,56 @@ cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* h
   auto k = vec ? pcg_direction_kernel<true> : pcg_direction_kernel<false>;
   const cudaError_t err = launch_pdl(k, dim3(vec_grid()), dim3(VT), 0, s, st, it, hist, n_L, m, d,
                                      r, x, p, pprev, pout, Ap, mask, own, part, rev, xmode);
+  count_launch();
+  return err;
+}
+
+}  // namespace hxf
+
+namespace hxf {
+
+int pcg_step_grid() { return num_sms(); }
+
+bool pcg_step_fusable(int64_t n_L, const double* d, const double* r, double* x, const double* p,
+                      const double* pprev, double* pout, double* Ap) {
+  static const bool off = [] {
+    const char* v = std::getenv("HXF_PCG_FUSED");
+    return v && v[0] == '0';
+  }();
+  static const bool coop = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev);
+    return v != 0;
+  }();
+  return !off && coop && grid_cap() == 0 && (n_L % 2) == 0 && n_L * 3 < (int64_t(1) << 31) && aligned16(d) && aligned16(r) &&
+         aligned16(x) && aligned16(p) && aligned16(pprev) && aligned16(pout) && aligned16(Ap);
+}
+
+cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L, int m,
+                            const double* d, double* r, double* x, const double* p,
+                            const double* pprev, double* pout, double* Ap, const uint32_t* mask,
+                            double* part, int rev, int xmode) {
+  static const int unroll = [] {
+    const char* v = std::getenv("HXF_STEP_U");
+    return v ? std::atoi(v) : 1;
+  }();
+  auto kern = unroll == 2 ? pcg_step_kernel<2> : pcg_step_kernel<1>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
+  if (attr != cudaSuccess) return attr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pcg_step_grid());
+  cfg.blockDim = dim3(ST_NT);
+  cfg.dynamicSmemBytes = ST_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barrier)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, st, it, hist, n_L, m, d, r, x,
+                                             p, pprev, pout, Ap, mask, part, rev, xmode);
   count_launch();
   return err;
 }
