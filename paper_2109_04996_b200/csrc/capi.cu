@@ -101,16 +101,16 @@ bool pdl_apply_disabled() {
 
 bool dmmaeo_enabled(int P, int ncomp) {
   // measured (BP5 / BP6 ~1e7 DOFs, K1): the even-odd tensor-core kernel wins
-  // from p = 12 (one component: p = 12 290 vs 289 us, p = 15 243 vs 314 us)
-  // and p = 11 (three components: 324 vs 374 us, p = 15 234 vs 410 us); the
-  // line / pencil kernels stay ahead below
+  // from p = 13 (one component: p = 13 294 vs 366 us, p = 15 201 vs 314 us;
+  // p = 12 311 vs 290) and p = 11 (three components: 321 vs 374 us, p = 15
+  // 195 vs 410 us); the line / pencil kernels stay ahead below
   static const int mode = [] {
     const char* v = std::getenv("HXF_DMMAEO");
     return v ? std::atoi(v) : 1;
   }();
   if (mode == 0) return false;
   if (mode == 2) return true;  // every P = 9..16 (A/B)
-  return ncomp == 1 ? P >= 13 : P >= 12;
+  return ncomp == 1 ? P >= 14 : P >= 12;
 }
 
 bool dmma_pad_disabled() {

@@ -14,20 +14,24 @@
 // (op_line.cuh) it replaces is issue-bound at these orders (BP5 p = 12..15 at
 // 0.32-0.41 of HBM, issue-active 23 %).
 //
-// One element (per component) at a time per CTA of 8 warps, 2 CTAs per SM.
+// One element (per component) at a time per CTA of N warps (one per plane
+// and row: no warp carries two units across a barrier), one CTA per SM.
 // Lane l: g = l>>2, t = l&3 (the mma fragment coordinates).  "dist X" of
 // plane k: the lane owns the 8 points (k, R_r, C_q), rows R = {g, N-1-g} and
 // columns C = {2t, 2t+1, N-1-2t, N-2-2t} — exactly the rows / columns an
 // even-odd product emits for output pair (o, N-1-o), so the x-, y- and
 // (through shared memory) z-derivatives of a point meet in one lane.  Warp w
-// owns planes {w, w+8} and rows {w, w+8} (for the z-direction, "dist Z").
+// owns plane w and (for the z-direction, "dist Z") row w.
 //   B0  the element's x slab landed (cp.async, issued one item ahead)
-//   1   z-derivative per owned row (dist Z) -> slab Z
-//   2   per owned plane: x- and y-derivatives in registers, QFunction with
-//       the factors from global memory (L2-prefetched one element ahead by a
-//       bulk prefetch); V0 -> slab U (in place), V1 -> slab B, V2 -> slab Z
-//   3   z^T per owned row into registers; x^T + y^T per owned plane -> slab U
-//       (in place); then the next item's gather into slab B, and the scatter:
+//   1   z-derivative of the warp's row (dist Z) -> slab Z
+//   2   x- and y-derivatives of the warp's plane in registers, QFunction with
+//       the factors staged in shared memory (N <= 14: one bulk copy set per
+//       element, issued when the previous element's QFunction consumed its
+//       factors, the element after that L2-prefetched) or read from L2
+//       (N = 15, 16: bulk-prefetched one element ahead); V0 -> slab U (in
+//       place), V1 -> slab B, V2 -> slab Z
+//   3   x^T + y^T of the plane -> slab U (in place); then the next item's
+//       gather into slab B, z^T of the row in registers and the scatter:
 //       y = U + z^T in dist Z, FP64 RED
 // Slabs are [k][j][16] (rows padded to 16 doubles) with the column XOR-
 // swizzled by 4 * (perm(j & 3) ^ perm(k & 3)), perm swapping the two bits:
@@ -40,9 +44,6 @@
 #include "op_dmma.cuh"  // dmma()
 #include "pcg_device.cuh"
 
-#ifndef HXF_EO_MINB
-#define HXF_EO_MINB 2
-#endif
 namespace hxf {
 
 template <int N_, int NC_>
@@ -51,10 +52,18 @@ struct EoTraits {
   static constexpr int H = (N_ + 1) / 2, HI = N_ / 2;
   static constexpr bool ODD = (N_ & 1) != 0;
   static_assert(N_ >= 9 && N_ <= 16, "even-odd halves of 5..8 fit one 8x8 DMMA tile");
-  static constexpr int NW = 8, NT = 256;
+  // one warp per plane (x / y products, QFunction, x^T / y^T) and per row
+  // (z and z^T products): no warp holds two units across a barrier
+  static constexpr int NW = N_, NT = 32 * N_;
   static constexpr int SLAB = N_ * N_ * 16;  // doubles (rows padded to 16)
   static constexpr int QDS = 6 * N3;         // geometric factors per element
-  static constexpr int SMEM_BYTES = 3 * SLAB * 8;
+  // QS: the element's factors staged in shared memory by bulk copies (TMA
+  // engine), issued as soon as the previous element's QFunction consumed
+  // them; N = 15, 16 do not fit (162 / 196 KB) and read them from L2 instead
+  static constexpr int SLABS_BYTES = 3 * SLAB * 8;
+  static constexpr bool QS = SLABS_BYTES + QDS * 8 + 4096 <= 227 * 1024;
+  static constexpr int SMEM_BYTES = SLABS_BYTES + (QS ? QDS * 8 : 0);
+  static constexpr int MINB = 1;  // (~128-166 registers per thread)
   __device__ static __forceinline__ int perm(int x) { return ((x & 1) << 1) | ((x >> 1) & 1); }
   __device__ static __forceinline__ int off(int k, int j, int i) {
     return (k * N_ + j) * 16 + (i ^ (4 * (perm(j & 3) ^ perm(k & 3))));
@@ -75,7 +84,7 @@ __device__ __forceinline__ double2 ld_stream2(const double* p) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __grid_constant__ OpParams prm) {
+__global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_constant__ OpParams prm) {
   constexpr int N = T::N, NN = T::NN, N3 = T::N3, H = T::H, HI = T::HI, NC = T::NC, NT = T::NT;
   extern __shared__ __align__(128) double eo_smem[];
   __shared__ double red_scratch[NT / 32 + 1];
@@ -272,21 +281,50 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
     }
   };
 
+  __shared__ __align__(8) uint64_t qbar;
+  double* SQ = eo_smem + 3 * T::SLAB;  // staged factors (T::QS)
+  auto issue_qdata = [&](int64_t e) {  // bulk copies of <= 32 KB (16-byte multiples)
+    constexpr uint32_t total = T::QDS * 8, chunk = 32768;
+    mbar_arrive_expect_tx(&qbar, total);
+    const uint64_t pol = l2_evict_first_policy();
+    const char* src = reinterpret_cast<const char*>(prm.qd + e * T::QDS);
+    char* dst = reinterpret_cast<char*>(SQ);
+#pragma unroll 1
+    for (uint32_t o = 0; o < total; o += chunk)
+      bulk_g2s(dst + o, src + o, total - o < chunk ? total - o : chunk, &qbar, pol);
+  };
+  const int k = w, j = w;  // this warp's plane and row
   double dot_acc = 0.0;
   int64_t s = blockIdx.x;
   Geo cur{};
+  if (T::QS && tid == 0) {
+    mbar_init(&qbar, 1);
+    fence_mbar_init();
+  }
   if (s < nsteps) {
     cur = geometry(s);
-    if (tid == 0) bulk_prefetch_l2(prm.qd + cur.e * T::QDS, (uint32_t)(T::QDS * 8));
+    if (tid == 0 && !(prm.ablate & 4)) {
+      if constexpr (T::QS) {
+        issue_qdata(cur.e);
+        if (s + G < nsteps) bulk_prefetch_l2(prm.qd + elem(s + G) * T::QDS, (uint32_t)(T::QDS * 8));
+      } else {
+        bulk_prefetch_l2(prm.qd + cur.e * T::QDS, (uint32_t)(T::QDS * 8));
+      }
+    }
     issue_gather(cur, 0, SU);
   }
+  int it = 0;
 #pragma unroll 1
-  for (; s < nsteps; s += G) {
+  for (; s < nsteps; s += G, ++it) {
     const bool has_next = s + G < nsteps;
-    // factors of the next element: HBM -> L2 while this one computes
-    if (tid == 0 && has_next && !(prm.ablate & 4)) bulk_prefetch_l2(prm.qd + elem(s + G) * T::QDS, (uint32_t)(T::QDS * 8));
+    // factors ahead: HBM -> L2 (staged: the element after next, whose bulk
+    // copy is issued during the next element)
+    if (tid == 0 && !(prm.ablate & 4)) {
+      const int64_t pf = s + (T::QS ? 2 : 1) * G;
+      if (pf < nsteps) bulk_prefetch_l2(prm.qd + elem(pf) * T::QDS, (uint32_t)(T::QDS * 8));
+    }
     Geo nxt = cur;
-    const double* qe = prm.qd + cur.e * T::QDS;
+    const double* qe = T::QS ? SQ : prm.qd + cur.e * T::QDS;
 #pragma unroll 1
     for (int c = 0; c < NC; ++c) {
       double* yc = prm.y + c * prm.n_L;
@@ -296,95 +334,95 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
 
       double fe[2], fo[2];
       frags(0, fe, fo);
-      // ---- 1: z-derivative of the owned rows (dist Z) -> slab Z ----
-#pragma unroll 1
-      for (int jj = 0; jj < 2; ++jj) {
-        const int j = w + 8 * jj;
-        if (j < N) {
-          double out[8];
-          rowop([&](int b, int col) { return SU[T::off(b, j, col)]; }, fe, fo, out);
-          st_slots_z(SZ, j, out);
-        }
+      // ---- 1: z-derivative of this warp's row (dist Z) -> slab Z ----
+      {
+        double out[8];
+        rowop([&](int b, int col) { return SU[T::off(b, j, col)]; }, fe, fo, out);
+        st_slots_z(SZ, j, out);
       }
       __syncthreads();  // B1: G2 complete
 
-      // ---- 2: x / y derivatives of the owned planes, QFunction (qfunction.cpp:135-162) ----
+      // ---- 2: x / y derivatives of this warp's plane, QFunction (qfunction.cpp:135-162) ----
       double energy = 0.0;
-#pragma unroll 1
-      for (int kk = 0; kk < 2; ++kk) {
-        const int k = w + 8 * kk;
-        if (k < N) {
-          // factors of step st = (row r = st >> 1, column pair hp = st & 1):
-          // software-pipelined one step ahead (step 0 lands under the DMMA work)
-          auto load_sv = [&](int st, double (*sv)[2]) {
-            const int R = (st >> 1) ? R1 : R0, hp = st & 1;
-            const double* qp = qe + k * NN + R * N;
+      {
+        // factors of step st = (row r = st >> 1, column pair hp = st & 1)
+        auto load_sv = [&](int st, double (*sv)[2]) {
+          const int R = (st >> 1) ? R1 : R0, hp = st & 1;
+          const double* qp = qe + k * NN + R * N;
 #pragma unroll
-            for (int m = 0; m < 6; ++m) {
-              if (prm.ablate & 4) {  // measurement-only: no factor traffic
-                sv[m][0] = sv[m][1] = 1.0 + m;
-              } else if constexpr (!T::ODD) {  // (odd N: rows of the factor planes are not 16-byte aligned)
-                const double2 a = __ldg(reinterpret_cast<const double2*>(qp + m * N3 + (hp ? C3 : C0)));
-                sv[m][0] = a.x;
-                sv[m][1] = a.y;
-              } else {
-                sv[m][0] = __ldg(qp + m * N3 + (hp ? C3 : C0));
-                sv[m][1] = __ldg(qp + m * N3 + (hp ? C2 : C1));
-              }
+          for (int m = 0; m < 6; ++m) {
+            if (prm.ablate & 4) {  // measurement-only: no factor traffic
+              sv[m][0] = sv[m][1] = 1.0 + m;
+            } else if constexpr (T::QS && !T::ODD) {
+              const double2 a = *reinterpret_cast<const double2*>(qp + m * N3 + (hp ? C3 : C0));
+              sv[m][0] = a.x;
+              sv[m][1] = a.y;
+            } else if constexpr (T::QS) {
+              sv[m][0] = qp[m * N3 + (hp ? C3 : C0)];
+              sv[m][1] = qp[m * N3 + (hp ? C2 : C1)];
+            } else if constexpr (!T::ODD) {  // (odd N: factor rows not 16-byte aligned)
+              const double2 a = __ldg(reinterpret_cast<const double2*>(qp + m * N3 + (hp ? C3 : C0)));
+              sv[m][0] = a.x;
+              sv[m][1] = a.y;
+            } else {
+              sv[m][0] = __ldg(qp + m * N3 + (hp ? C3 : C0));
+              sv[m][1] = __ldg(qp + m * N3 + (hp ? C2 : C1));
             }
-          };
-          double sva[6][2], svb[6][2];
-          load_sv(0, sva);
-          double g0[8], g1[8];
-          colop(SU, k, fe, fo, g0);
-          rowop([&](int b, int col) { return SU[T::off(k, b, col)]; }, fe, fo, g1);
-          __syncwarp();  // every lane's reads of plane k before V0 replaces it
-#pragma unroll
-          for (int st = 0; st < 4; ++st) {
-            const int r = st >> 1, hp = st & 1;
-            const int R = r ? R1 : R0;
-            double (*sv)[2] = (st & 1) ? svb : sva;
-            if (st < 3) load_sv(st + 1, (st & 1) ? sva : svb);
-            const int lo = slo(hp), hi = shi(hp);
-            double z[2], v0[2], v1[2], v2[2];
-            ld_pair(SZ, k, R, hp, z[0], z[1]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int sl = r * 4 + (h ? hi : lo);
-              const double a0 = g0[sl], a1 = g1[sl], a2 = z[h];
-              const double s00 = sv[0][h], s01 = sv[1][h], s02 = sv[2][h];
-              const double s11 = sv[3][h], s12 = sv[4][h], s22 = sv[5][h];
-              v0[h] = s00 * a0 + s01 * a1 + s02 * a2;
-              v1[h] = s01 * a0 + s11 * a1 + s12 * a2;
-              v2[h] = s02 * a0 + s12 * a1 + s22 * a2;
-              // p.(A p) over free nodes = sum_points grad u . S grad u
-              if (valid(sl)) energy += a0 * v0[h] + a1 * v1[h] + a2 * v2[h];
-            }
-            const bool vl = valid(r * 4 + lo), vh = valid(r * 4 + hi);
-            st_pair(SU, k, R, hp, v0[0], v0[1], vl, vh);
-            st_pair(SB, k, R, hp, v1[0], v1[1], vl, vh);
-            st_pair(SZ, k, R, hp, v2[0], v2[1], vl, vh);
           }
+        };
+        double sva[6][2], svb[6][2];
+        if constexpr (T::QS) {
+          if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
+        }
+        load_sv(0, sva);
+        double g0[8], g1[8];
+        colop(SU, k, fe, fo, g0);
+        rowop([&](int b, int col) { return SU[T::off(k, b, col)]; }, fe, fo, g1);
+        __syncwarp();  // every lane's reads of plane k before V0 replaces it
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+          const int r = st >> 1, hp = st & 1;
+          const int R = r ? R1 : R0;
+          double (*sv)[2] = (st & 1) ? svb : sva;
+          if (st < 3) load_sv(st + 1, (st & 1) ? sva : svb);
+          const int lo = slo(hp), hi = shi(hp);
+          double z[2], v0[2], v1[2], v2[2];
+          ld_pair(SZ, k, R, hp, z[0], z[1]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int sl = r * 4 + (h ? hi : lo);
+            const double a0 = g0[sl], a1 = g1[sl], a2 = z[h];
+            const double s00 = sv[0][h], s01 = sv[1][h], s02 = sv[2][h];
+            const double s11 = sv[3][h], s12 = sv[4][h], s22 = sv[5][h];
+            v0[h] = s00 * a0 + s01 * a1 + s02 * a2;
+            v1[h] = s01 * a0 + s11 * a1 + s12 * a2;
+            v2[h] = s02 * a0 + s12 * a1 + s22 * a2;
+            // p.(A p) over free nodes = sum_points grad u . S grad u
+            if (valid(sl)) energy += a0 * v0[h] + a1 * v1[h] + a2 * v2[h];
+          }
+          const bool vl = valid(r * 4 + lo), vh = valid(r * 4 + hi);
+          st_pair(SU, k, R, hp, v0[0], v0[1], vl, vh);
+          st_pair(SB, k, R, hp, v1[0], v1[1], vl, vh);
+          st_pair(SZ, k, R, hp, v2[0], v2[1], vl, vh);
         }
       }
       dot_acc += prm.coef * energy;
-      __syncthreads();  // B2: V0, V1, V2 complete
+      if (T::QS && c == NC - 1) fence_proxy_async_smem();  // factor reads before the refill
+      __syncthreads();  // B2: V0, V1, V2 complete; staged factors consumed
+      if (T::QS && c == NC - 1 && tid == 0 && has_next && !(prm.ablate & 4))
+        issue_qdata(elem(s + G));
 
       double te[2], to[2];
       frags(1, te, to);
-      // ---- 3: x^T + y^T of the owned planes -> slab U (in place) ----
-#pragma unroll 1
-      for (int kk = 0; kk < 2; ++kk) {
-        const int k = w + 8 * kk;
-        if (k < N) {
-          double ya[8], yb[8];
-          colop(SU, k, te, to, ya);
-          rowop([&](int b, int col) { return SB[T::off(k, b, col)]; }, te, to, yb);
+      // ---- 3: x^T + y^T of this warp's plane -> slab U (in place) ----
+      {
+        double ya[8], yb[8];
+        colop(SU, k, te, to, ya);
+        rowop([&](int b, int col) { return SB[T::off(k, b, col)]; }, te, to, yb);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) ya[q] += yb[q];
-          __syncwarp();  // every lane's reads of plane k of U before the sums replace it
-          st_slots_x(SU, k, ya);
-        }
+        for (int q = 0; q < 8; ++q) ya[q] += yb[q];
+        __syncwarp();  // every lane's reads of plane k of U before the sums replace it
+        st_slots_x(SU, k, ya);
       }
       __syncthreads();  // B3: x^T + y^T complete; slab B consumed
 
@@ -395,37 +433,33 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
         nxt = geometry(s + G);
         issue_gather(nxt, 0, SB);
       }
-      // ---- z^T of the owned rows (slab Z holds V2 until the next item's
+      // ---- z^T of this warp's row (slab Z holds V2 until the next item's
       //      phase 1) and the scatter in dist Z: y = coef (x^T + y^T + z^T),
       //      FP64 RED ----
-      const int f = prm.bnd_faces;
-#pragma unroll 1
-      for (int jj = 0; jj < 2; ++jj) {
-        const int j = w + 8 * jj;
-        if (j < N) {
-          double y2[8];
-          rowop([&](int b, int col) { return SZ[T::off(b, j, col)]; }, te, to, y2);
+      {
+        const int f = prm.bnd_faces;
+        double y2[8];
+        rowop([&](int b, int col) { return SZ[T::off(b, j, col)]; }, te, to, y2);
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int R = r ? R1 : R0;
-            double u[4];
-            ld_pair(SU, R, j, 0, u[0], u[1]);  // (dist Z: plane R, row j)
-            ld_pair(SU, R, j, 1, u[3], u[2]);
+        for (int r = 0; r < 2; ++r) {
+          const int R = r ? R1 : R0;
+          double u[4];
+          ld_pair(SU, R, j, 0, u[0], u[1]);  // (dist Z: plane R, row j)
+          ld_pair(SU, R, j, 1, u[3], u[2]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (!valid(4 * r + q)) continue;
-              const int C = Cq[q];
-              const double yv = prm.coef * (u[q] + y2[4 * r + q]);
-              bool cons = false;
-              if (cur.bnd) {
-                const int64_t ix = cur.ix0 + C, iy = cur.iy0 + j, iz = cur.iz0 + R;
-                cons = ((f & 1) && ix == 0) || ((f & 2) && ix == prm.NX - 1) ||
-                       ((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1) ||
-                       ((f & 16) && iz == 0) || ((f & 32) && iz == prm.NZ - 1);
-              }
-              // constrained rows (y = x) are preset by the caller
-              if (!cons && !(prm.ablate & 2)) red_add(yc + cur.base + C + prm.NX * j + NXY * R, yv);
+          for (int q = 0; q < 4; ++q) {
+            if (!valid(4 * r + q)) continue;
+            const int C = Cq[q];
+            const double yv = prm.coef * (u[q] + y2[4 * r + q]);
+            bool cons = false;
+            if (cur.bnd) {
+              const int64_t ix = cur.ix0 + C, iy = cur.iy0 + j, iz = cur.iz0 + R;
+              cons = ((f & 1) && ix == 0) || ((f & 2) && ix == prm.NX - 1) ||
+                     ((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1) ||
+                     ((f & 16) && iz == 0) || ((f & 32) && iz == prm.NZ - 1);
             }
+            // constrained rows (y = x) are preset by the caller
+            if (!cons && !(prm.ablate & 2)) red_add(yc + cur.base + C + prm.NX * j + NXY * R, yv);
           }
         }
       }
@@ -435,7 +469,6 @@ __global__ void __launch_bounds__(T::NT, HXF_EO_MINB) op_dmmaeo_kernel(const __g
     }
     cur = nxt;
   }
-
   if (prm.dot_partials) {
     const double sum = block_sum<NT>(dot_acc, red_scratch);
     if (tid == 0) prm.dot_partials[blockIdx.x] = sum;

@@ -194,9 +194,10 @@ def test_apply_vs_oracle_across_orders(ctx, bp, p, dims):
     assert oracle.rel_max_diff(pr.apply(x), op.apply(x)) <= APPLY_TOL
 
 
-# even-odd FP64 tensor-core kernel (op_dmmaeo.cuh; dispatched for p >= 12 one
-# component, p >= 11 three): odd and even N = p+1, box-constrained sine
-# meshes; the lower orders of the list run the line / pencil kernels
+# even-odd FP64 tensor-core kernel (op_dmmaeo.cuh; dispatched for p >= 13 one
+# component, p >= 11 three): odd and even N = p+1, factors staged in shared
+# memory (N <= 14) or read from L2 (N = 15, 16), box-constrained sine meshes;
+# the lower orders of the list run the line / pencil kernels
 DMMAEO_CASES = [("bp5", 8, (2, 3, 2)), ("bp5", 9, (2, 2, 2)), ("bp5", 10, (2, 1, 2)),
                 ("bp5", 11, (1, 2, 2)), ("bp5", 12, (2, 1, 1)), ("bp5", 13, (1, 2, 1)),
                 ("bp5", 14, (1, 1, 2)), ("bp5", 15, (2, 1, 1)), ("bp6", 8, (2, 2, 1)),
@@ -249,9 +250,9 @@ KERNEL_FAMILIES = [
     ("bp1", 3, (5, 4, 3)),   # line, mass
     ("bp2", 4, (3, 3, 2)),   # line, mass, three components
     ("bp5", 1, (7, 6, 5)),   # line, 64-thread CTAs
-    ("bp5", 12, (2, 2, 2)),  # even-odd DMMA, odd N
-    ("bp5", 15, (2, 2, 1)),  # even-odd DMMA, even N
-    ("bp6", 11, (2, 1, 2)),  # even-odd DMMA, three components
+    ("bp5", 13, (2, 2, 2)),  # even-odd DMMA, staged factors
+    ("bp5", 15, (2, 2, 1)),  # even-odd DMMA, factors from L2
+    ("bp6", 12, (2, 1, 2)),  # even-odd DMMA, three components, odd N
 ]
 
 
