@@ -44,6 +44,9 @@
 #include "op_dmma.cuh"  // dmma()
 #include "pcg_device.cuh"
 
+#ifndef HXF_EO_MINB  // CTAs per SM the register budget targets (0: two for N <= 11)
+#define HXF_EO_MINB 1
+#endif
 namespace hxf {
 
 template <int N_, int NC_>
@@ -63,7 +66,12 @@ struct EoTraits {
   static constexpr int SLABS_BYTES = 3 * SLAB * 8;
   static constexpr bool QS = SLABS_BYTES + QDS * 8 + 4096 <= 227 * 1024;
   static constexpr int SMEM_BYTES = SLABS_BYTES + (QS ? QDS * 8 : 0);
-  static constexpr int MINB = 1;  // (~128-166 registers per thread)
+  // one CTA per SM (~128-166 registers per thread).  Measured with two (N <=
+  // 11, 96 / 80 registers, small spills; HXF_EO_MINB=0 at build time): BP5
+  // p = 8 / 9 652 -> 512 / 543 -> 447 us but p = 10 388 -> 425 us — still far
+  // behind the line kernel (205 / 257 / 264 us) there, so not dispatched
+  static constexpr int MINB = HXF_EO_MINB > 0 ? HXF_EO_MINB
+                              : ((N_ <= 11 && 2 * (SMEM_BYTES + 3072) <= 228 * 1024) ? 2 : 1);
   __device__ static __forceinline__ int perm(int x) { return ((x & 1) << 1) | ((x >> 1) & 1); }
   __device__ static __forceinline__ int off(int k, int j, int i) {
     return (k * N_ + j) * 16 + (i ^ (4 * (perm(j & 3) ^ perm(k & 3))));
@@ -370,11 +378,14 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
             }
           }
         };
+        // (global factors: software-pipelined one step ahead, step 0 under the
+        // DMMA work; staged factors: loaded at their step, fewer live registers)
         double sva[6][2], svb[6][2];
         if constexpr (T::QS) {
           if (c == 0 && !(prm.ablate & 4)) mbar_wait(&qbar, (uint32_t)(it & 1));
+        } else {
+          load_sv(0, sva);
         }
-        load_sv(0, sva);
         double g0[8], g1[8];
         colop(SU, k, fe, fo, g0);
         rowop([&](int b, int col) { return SU[T::off(k, b, col)]; }, fe, fo, g1);
@@ -384,7 +395,11 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
           const int r = st >> 1, hp = st & 1;
           const int R = r ? R1 : R0;
           double (*sv)[2] = (st & 1) ? svb : sva;
-          if (st < 3) load_sv(st + 1, (st & 1) ? sva : svb);
+          if constexpr (T::QS) {
+            load_sv(st, sv);
+          } else {
+            if (st < 3) load_sv(st + 1, (st & 1) ? sva : svb);
+          }
           const int lo = slo(hp), hi = shi(hp);
           double z[2], v0[2], v1[2], v2[2];
           ld_pair(SZ, k, R, hp, z[0], z[1]);
