@@ -54,6 +54,11 @@ int64_t hxf_launch_count(void);
  * full-size configurations run.  Returns the previous cap.  Affects launches
  * made (and graphs captured) after the call. */
 int hxf_debug_set_grid_cap(int cap);
+/* Measurement knob: `on` != 0 makes the fused PCG step kernel record per-CTA
+ * %globaltimer stamps (start, phase-1 end, after the grid barrier, phase-2
+ * end) of its following launches; `out` (4 x 1024 uint64, or NULL) receives
+ * the stamps of the last launch.  Current device. */
+int hxf_debug_step_timestamps(int on, unsigned long long* out);
 
 /* ---- context: one CUDA device (+ optional NCCL communicator) ----------- */
 int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out);

@@ -99,6 +99,17 @@ bool pdl_apply_disabled() {
   return off;
 }
 
+// HXF_STEP_APZ=1: the step kernel zeroes Ap in phase 1 and the DMMA kernel
+// stores Ap = p on the constrained rows (measured and dropped: C3 CG iteration
+// 156.4 -> 161.2 us, K1 89 -> 93 us; the zeros leave L2 before K1 adds into them)
+bool step_ap_zero() {
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_STEP_APZ");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 bool dmmaeo_enabled(int P, int ncomp) {
   // measured (BP5 / BP6 ~1e7 DOFs, K1): the even-odd tensor-core kernel wins
   // from p = 13 (one component: p = 13 294 vs 366 us, p = 15 201 vs 314 us;
@@ -308,20 +319,28 @@ cudaStream_t pick_stream(hxf_op* op, void* stream) {
 // y = op x on the device (y preset here unless zero_y is false; the kernel
 // REDs into it).  PCG (st != nullptr): per-CTA partials of p.(A p) go to
 // dot_part and the last CTA of the last pass derives alpha into *st.
+// Does the operator kernel store y = x on the constrained rows itself when
+// asked (prm.cons_store)?  The DMMA kernel (single domain, p = 7 diffusion).
+bool k1_stores_cons(const hxf_op* op) {
+  return op->P == 8 && !op->interp && op->beta == 0.0 && !op->d_own && op->cons_mode != 0 &&
+         op_kernel_choice() == 0;
+}
+
+// k1_cons (PCG, fused step): y is all zero and the kernel stores y = x on the
+// constrained rows (no preset of them by the step kernel)
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
                   int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr,
-                  bool halo = true, int rev = 0) {
+                  bool halo = true, int rev = 0, bool k1_cons = false) {
   // single-domain p = 7 collocated diffusion: y zeroed by a write-only memset
   // and the DMMA kernel stores y = x on the constrained rows it gathers
   // (instead of the read-x/write-y init_y pass)
-  const bool cons_store = zero_y && op->P == 8 && !op->interp && op->beta == 0.0 && !op->d_own &&
-                          op->cons_mode != 0 && op_kernel_choice() == 0;
+  const bool cons_store = zero_y && k1_stores_cons(op);
   if (cons_store)
     ck(cudaMemsetAsync(y, 0, sizeof(double) * op->n_L * op->m, s), "y memset");
   else if (zero_y)
     ck(launch_init_y(s, op->n_L, op->m, x, y, op->d_mask, op->d_own), "init_y");
   OpParams prm{};
-  prm.cons_store = cons_store ? 1 : 0;
+  prm.cons_store = (cons_store || k1_cons) ? 1 : 0;
   // single apply: the kernel's factor copy and setup overlap the memset's tail
   // (it waits in griddepcontrol.wait before touching y); measured 90.6 -> 88.4 us
   prm.pdl = cons_store && !pdl_apply_disabled() ? 1 : 0;
@@ -510,20 +529,25 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
   const int serp = serpentine() ? 1 : 0, odd = it & 1;
   int nparts = 0;
   if (ps.timed) record(op->ev[2 * (it - 1)]);
+  const int xmode = !xb ? 0 : ((it & 1) ? 1 : 2);
+  double* pout = !xb ? pA : ((it & 1) ? pB : pA);
+  // single domain: update + direction as one cooperative kernel (grid barrier
+  // between them, z kept on chip) — no all-reduce has to sit in between; with
+  // the DMMA operator kernel storing Ap = p on the constrained rows itself,
+  // the step kernel zeroes Ap right after reading it and writes no preset
+  const bool fused = !op->comm && !op->d_own &&
+                     pcg_step_fusable(op->n_L, ps.dinv, r, ps.dx, p, xmode == 2 ? pA : nullptr, pout, Ap);
+  const bool k1c = fused && k1_stores_cons(op) && step_ap_zero();
   // Ap was preset by the init / direction kernel: no memset pass here
   // partitioned: the interface sum-exchange of Ap is part of the apply
   // (overlapped with the interior elements where the kernel allows)
   device_apply(op, p, Ap, s, op->d_part, &nparts, &op->d_state->stop, /*zero_y=*/false,
-               op->d_state, /*halo=*/true, serp & (odd ^ 1));
+               op->d_state, /*halo=*/true, serp & (odd ^ 1), k1c);
   if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time (single GPU: K1 alone)
-  const int xmode = !xb ? 0 : ((it & 1) ? 1 : 2);
-  double* pout = !xb ? pA : ((it & 1) ? pB : pA);
-  // single domain: update + direction as one cooperative kernel (grid barrier
-  // between them, z kept on chip) — no all-reduce has to sit in between
-  if (!op->comm && !op->d_own &&
-      pcg_step_fusable(op->n_L, ps.dinv, r, ps.dx, p, xmode == 2 ? pA : nullptr, pout, Ap)) {
+  if (fused) {
     ck(pcg_launch_step(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,
-                       xmode == 2 ? pA : nullptr, pout, Ap, op->d_mask, vpart, serp & odd, xmode),
+                       xmode == 2 ? pA : nullptr, pout, Ap, op->d_mask, vpart, serp & odd, xmode,
+                       k1c),
        "pcg step");
     return;
   }
@@ -651,6 +675,10 @@ int hxf_debug_set_grid_cap(int cap) {
   const int old = g_grid_cap.load();
   g_grid_cap.store(cap > 0 ? cap : 0);
   return old;
+}
+
+int hxf_debug_step_timestamps(int on, unsigned long long* out) {
+  return guarded([&] { pcg_step_timestamps(on, out); });
 }
 
 int hxf_context_create(int device, void* nccl_comm, hxf_ctx** out) {

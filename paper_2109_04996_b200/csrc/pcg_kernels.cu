@@ -373,6 +373,14 @@ __global__ void __launch_bounds__(VT, 4)
 // Saves the r and 1/d re-reads of the cached pairs (2/3 of the vectors at C3)
 // and one kernel boundary per iteration.
 constexpr int ST_NT = 1024;
+// measurement-only phase timestamps of the fused step kernel (tools/step_phases.py)
+__device__ unsigned long long g_step_ts[4][1024];
+__device__ int g_step_ts_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int ST_SMEM = 192 * 1024;
 
 __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
@@ -393,16 +401,20 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
   __syncthreads();
 }
 
-template <int ST_U>  // grid-stride steps per loop trip (loads of all of them first)
+// ST_CS: the x and r stores evict-first (written back to HBM while this kernel
+// runs instead of being flushed under the next operator kernel)
+template <int ST_U, bool ST_CS>  // ST_U: grid-stride steps per loop trip (loads of all of them first)
 __global__ void __launch_bounds__(ST_NT, 1)
     pcg_step_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                     const double* __restrict__ d, double* __restrict__ r, double* __restrict__ x,
                     const double* p, const double* pprev, double* pout, double* __restrict__ Ap,
-                    const uint32_t* cons_mask, double* part, int rev, int xmode) {
+                    const uint32_t* cons_mask, double* part, int rev, int xmode, int ap_zero) {
   extern __shared__ double2 zc[];
   __shared__ double scratch[ST_NT / 32];
   constexpr int zcap = ST_SMEM / 16;
   if (st->stop) return;  // stopped in an earlier iteration
+  const bool ts = g_step_ts_on == it && threadIdx.x == 0;  // (iteration to stamp)
+  if (ts) g_step_ts[0][blockIdx.x] = gtimer();
   const double pap = st->red[0];
   const double rho = st->rho;
   const int G = gridDim.x;
@@ -473,7 +485,8 @@ __global__ void __launch_bounds__(ST_NT, 1)
       double2 v = rv[u];
       v.x -= alpha * av[u].x;
       v.y -= alpha * av[u].y;
-      r2[k[u]] = v;
+      if (ST_CS) __stcs(r2 + k[u], v); else r2[k[u]] = v;
+      if (ap_zero) a2[k[u]] = make_double2(0.0, 0.0);  // the next operator kernel's RED target
       const double2 z = make_double2(v.x * dv[u].x, v.y * dv[u].y);
       rr += v.x * v.x + v.y * v.y;
       rz += v.x * z.x + v.y * z.y;
@@ -489,7 +502,9 @@ __global__ void __launch_bounds__(ST_NT, 1)
       part[G + blockIdx.x] = s1;
     }
   }
+  if (ts) g_step_ts[1][blockIdx.x] = gtimer();
   grid_barrier(&st->gbar[0], &st->gbar[1]);
+  if (ts) g_step_ts[2][blockIdx.x] = gtimer();
   __shared__ double tot[2];
   {
     const double trr = pcg_sum_partials<ST_NT>(part, G, scratch);
@@ -546,7 +561,7 @@ __global__ void __launch_bounds__(ST_NT, 1)
         }
         xn.x = fma(alpha, pv[u].x, xn.x);
         xn.y = fma(alpha, pv[u].y, xn.y);
-        x2[k[u]] = xn;
+        if (ST_CS) __stcs(x2 + k[u], xn); else x2[k[u]] = xn;
       }
       if (stop) continue;
       double2 pn;
@@ -556,11 +571,12 @@ __global__ void __launch_bounds__(ST_NT, 1)
       int64_t node = 2 * (int64_t)k[u];
       if (m > 1) node -= (node / n_L) * n_L;
       const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
-      a2[k[u]] = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
+      if (!ap_zero) a2[k[u]] = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
       if (w & 1u) cc += pn.x * pn.x;
       if (w & 2u) cc += pn.y * pn.y;
     }
   }
+  if (ts) g_step_ts[3][blockIdx.x] = gtimer();
   const double sc = block_sum<ST_NT>(cc, scratch);
   if (threadIdx.x == 0) part[2 * G + blockIdx.x] = sc;
   if (!pcg_last_cta(&st->counter[2])) return;
@@ -669,6 +685,12 @@ namespace hxf {
 
 int pcg_step_grid() { return num_sms(); }
 
+// measurement only: per-CTA phase timestamps of the next fused step launches
+void pcg_step_timestamps(int on, unsigned long long* out /* 4 x 1024, or nullptr */) {
+  cudaMemcpyToSymbol(g_step_ts_on, &on, sizeof on);
+  if (out) cudaMemcpyFromSymbol(out, g_step_ts, sizeof(unsigned long long) * 4 * 1024);
+}
+
 bool pcg_step_fusable(int64_t n_L, const double* d, const double* r, double* x, const double* p,
                       const double* pprev, double* pout, double* Ap) {
   static const bool off = [] {
@@ -688,12 +710,17 @@ bool pcg_step_fusable(int64_t n_L, const double* d, const double* r, double* x, 
 cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L, int m,
                             const double* d, double* r, double* x, const double* p,
                             const double* pprev, double* pout, double* Ap, const uint32_t* mask,
-                            double* part, int rev, int xmode) {
+                            double* part, int rev, int xmode, bool ap_zero) {
   static const int unroll = [] {
     const char* v = std::getenv("HXF_STEP_U");
     return v ? std::atoi(v) : 1;
   }();
-  auto kern = unroll == 2 ? pcg_step_kernel<2> : pcg_step_kernel<1>;
+  static const bool cs = [] {  // measured: C3 CG iteration 156.7 -> 155.9 us
+    const char* v = std::getenv("HXF_STEP_CS");
+    return !(v && v[0] == '0');
+  }();
+  auto kern = unroll == 2 ? (cs ? pcg_step_kernel<2, true> : pcg_step_kernel<2, false>)
+                          : (cs ? pcg_step_kernel<1, true> : pcg_step_kernel<1, false>);
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
   if (attr != cudaSuccess) return attr;
@@ -708,7 +735,8 @@ cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, st, it, hist, n_L, m, d, r, x,
-                                             p, pprev, pout, Ap, mask, part, rev, xmode);
+                                             p, pprev, pout, Ap, mask, part, rev, xmode,
+                                             ap_zero ? 1 : 0);
   count_launch();
   return err;
 }

@@ -29,13 +29,16 @@ cudaError_t pcg_launch_direction(cudaStream_t s, PcgState* st, int it, double* h
 // Fused update + direction (single domain, no owner mask, 16-byte aligned
 // vectors, even n_L): one persistent cooperative kernel per iteration, a grid
 // barrier between the two phases; the z = r/d of each CTA's chunk stays in
-// shared memory across it.  Returns cudaErrorNotSupported where it does not apply.
+// shared memory across it.  ap_zero: Ap is zeroed in phase 1 right after it is
+// read (the next operator kernel stores Ap = p on the constrained rows itself)
+// and phase 2 writes no Ap preset.
 bool pcg_step_fusable(int64_t n_L, const double* d, const double* r, double* x, const double* p,
                       const double* pprev, double* pout, double* Ap);
 cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, int64_t n_L, int m,
                             const double* d, double* r, double* x, const double* p,
                             const double* pprev, double* pout, double* Ap, const uint32_t* mask,
-                            double* part, int rev, int xmode);
+                            double* part, int rev, int xmode, bool ap_zero = false);
 int pcg_step_grid();  // CTAs of the fused kernel (partials it writes: 3 per CTA)
+void pcg_step_timestamps(int on, unsigned long long* out);  // measurement only
 
 }  // namespace hxf
