@@ -403,7 +403,9 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
 
 // ST_CS: the x and r stores evict-first (written back to HBM while this kernel
 // runs instead of being flushed under the next operator kernel)
-template <int ST_U, bool ST_CS>  // ST_U: grid-stride steps per loop trip (loads of all of them first)
+// ST_U / ST_U2: grid-stride steps per loop trip of phase 1 / 2 (loads of all
+// of them first: phase 2 of an odd iteration has one global load per step)
+template <int ST_U, int ST_U2, bool ST_CS>
 __global__ void __launch_bounds__(ST_NT, 1)
     pcg_step_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                     const double* __restrict__ d, double* __restrict__ r, double* __restrict__ x,
@@ -529,11 +531,11 @@ __global__ void __launch_bounds__(ST_NT, 1)
   const double2* pp2 = reinterpret_cast<const double2*>(xmode == 2 ? pprev : p);
   double2* po2 = reinterpret_cast<double2*>(pout);
   double cc = 0.0;
-  for (int j0 = nj - 1; j0 >= 0; j0 -= ST_U) {
-    int k[ST_U];
-    double2 pv[ST_U], xv[ST_U], qv[ST_U], z[ST_U];
+  for (int j0 = nj - 1; j0 >= 0; j0 -= ST_U2) {
+    int k[ST_U2];
+    double2 pv[ST_U2], xv[ST_U2], qv[ST_U2], z[ST_U2];
 #pragma unroll
-    for (int u = 0; u < ST_U; ++u) {
+    for (int u = 0; u < ST_U2; ++u) {
       const int j = j0 - u;
       k[u] = j >= 0 ? pair_at(j) : -1;
       if (k[u] < 0) continue;
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(ST_NT, 1)
       }
     }
 #pragma unroll
-    for (int u = 0; u < ST_U; ++u) {
+    for (int u = 0; u < ST_U2; ++u) {
       if (k[u] < 0) continue;
       if (xupd) {
         double2 xn = xv[u];
@@ -711,16 +713,13 @@ cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, 
                             const double* d, double* r, double* x, const double* p,
                             const double* pprev, double* pout, double* Ap, const uint32_t* mask,
                             double* part, int rev, int xmode, bool ap_zero) {
-  static const int unroll = [] {
-    const char* v = std::getenv("HXF_STEP_U");
-    return v ? std::atoi(v) : 1;
-  }();
+  // (measured, C3 CG iteration: phase 1 / 2 unrolled 1/2 158.6 us, 2/2 158.1,
+  // 1/4 178.3 (spills) vs 1/1 156.8 — kept 1/1)
   static const bool cs = [] {  // measured: C3 CG iteration 156.7 -> 155.9 us
     const char* v = std::getenv("HXF_STEP_CS");
     return !(v && v[0] == '0');
   }();
-  auto kern = unroll == 2 ? (cs ? pcg_step_kernel<2, true> : pcg_step_kernel<2, false>)
-                          : (cs ? pcg_step_kernel<1, true> : pcg_step_kernel<1, false>);
+  auto kern = cs ? pcg_step_kernel<1, 1, true> : pcg_step_kernel<1, 1, false>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
   if (attr != cudaSuccess) return attr;
