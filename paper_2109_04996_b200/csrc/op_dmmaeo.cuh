@@ -195,6 +195,19 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
       hi = S[T::off(k, R, C2)];
     }
   };
+  // reads only the valid slots (0 otherwise): in a phase that rewrites the
+  // points in place, an invalid slot aliases a point another lane rewrites
+  auto ld_pair_v = [&](const double* S, int k, int R, int hp, double& lo, double& hi, bool vlo,
+                       bool vhi) {
+    if ((hp == 0 || !T::ODD) && vlo && vhi) {
+      const double2 v = *reinterpret_cast<const double2*>(S + T::off(k, R, hp ? C3 : C0));
+      lo = v.x;
+      hi = v.y;
+    } else {
+      lo = vlo ? S[T::off(k, R, hp ? C3 : C0)] : 0.0;
+      hi = vhi ? S[T::off(k, R, hp ? C2 : C1)] : 0.0;
+    }
+  };
   // stores only the valid slots (an invalid slot aliases a point another
   // slot owns)
   auto st_pair = [&](double* S, int k, int R, int hp, double lo, double hi, bool vlo, bool vhi) {
@@ -305,9 +318,12 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
   double dot_acc = 0.0;
   int64_t s = blockIdx.x;
   Geo cur{};
-  if (T::QS && tid == 0) {
-    mbar_init(&qbar, 1);
-    fence_mbar_init();
+  if constexpr (T::QS) {
+    if (tid == 0) {
+      mbar_init(&qbar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();  // mbarrier initialised before any thread uses it
   }
   if (s < nsteps) {
     cur = geometry(s);
@@ -402,7 +418,7 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
           }
           const int lo = slo(hp), hi = shi(hp);
           double z[2], v0[2], v1[2], v2[2];
-          ld_pair(SZ, k, R, hp, z[0], z[1]);
+          ld_pair_v(SZ, k, R, hp, z[0], z[1], valid(r * 4 + lo), valid(r * 4 + hi));
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int sl = r * 4 + (h ? hi : lo);
