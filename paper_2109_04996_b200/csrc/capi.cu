@@ -110,6 +110,14 @@ bool step_ap_zero() {
   return on;
 }
 
+bool dmma3_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_DMMA3");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 bool dmmaeo_enabled(int P, int ncomp) {
   // measured (BP5 / BP6 ~1e7 DOFs, K1): the even-odd tensor-core kernel wins
   // from p = 13 (one component: p = 13 294 vs 366 us, p = 15 201 vs 314 us;

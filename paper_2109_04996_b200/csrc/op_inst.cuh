@@ -8,6 +8,7 @@
 #include "op_dmma.cuh"
 #include "op_line.cuh"
 #include "op_dmmaeo.cuh"
+#include "op_dmma3.cuh"
 
 namespace hxf {
 namespace {
@@ -165,6 +166,37 @@ cudaError_t run_dmmaeo(const OpParams& prm, cudaStream_t s, int* grid_out) {
   return err;
 }
 
+// BP6 p = 6, 7: the three components batched through every phase (op_dmma3.cuh)
+template <class T>
+cudaError_t run_dmma3(const OpParams& prm, cudaStream_t s, int* grid_out) {
+  static int max_ctas = -1;
+  auto kern = op_dmma3_kernel<T>;
+  if (max_ctas < 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int nb = 0;
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, T::NT, T::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    max_ctas = nb * num_sms();
+  }
+  if (!prm.D) return cudaErrorInvalidValue;
+  const int grid = capped_grid(prm.E, max_ctas);
+  if (grid_out) *grid_out = grid;
+  if (grid == 0) return cudaSuccess;
+  const cudaError_t err =
+      launch_pdl_if(pdl_enabled() || prm.pdl, kern, dim3(grid), dim3(T::NT), T::SMEM_BYTES, s, prm);
+  count_launch();
+  return err;
+}
+
+template <int NP>
+cudaError_t run_dmma3_gm(const OpParams& prm, cudaStream_t s, int* g) {
+  if (!prm.idx && prm.cons_mode != 2) return run_dmma3<Dmma3Traits<0, NP>>(prm, s, g);
+  return run_dmma3<Dmma3Traits<1, NP>>(prm, s, g);
+}
+
 template <int NC, int NW, int NP = 8>
 cudaError_t run_dmma_nw(const OpParams& prm, cudaStream_t s, int* g) {
   if constexpr (NP == 8 && NW == 4) {
@@ -216,6 +248,7 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
     // p = 7 collocated diffusion on the FP64 tensor cores
     if (qk == 1 && op_kernel_choice() == 0) {
       if (NC == 1) return run_dmma_gm<1>(prm, s, g);
+      if (NC == 3 && dmma3_enabled()) return run_dmma3_gm<8>(prm, s, g);
       if (NC == 3) return run_dmma_gm<3>(prm, s, g);
     }
   }
@@ -232,7 +265,7 @@ cudaError_t run_q(int NC, int qk, const OpParams& prm, const double* B, const do
     // pencil kernel (C4 BP6 p=6 40^3: K1 833 vs 1098 us); one component and
     // p = 4, 5 do not (fixed 8^3 tile cost per element: p=4 BP5 753 vs 297 us)
     if (qk == 1 && NC == 3 && op_kernel_choice() == 0 && !dmma_pad_disabled())
-      return run_dmma_gm<3, P>(prm, s, g);
+      return dmma3_enabled() ? run_dmma3_gm<P>(prm, s, g) : run_dmma_gm<3, P>(prm, s, g);
   }
   if constexpr (!INTERP) {
     // three components: the pencil kernel (even-odd; ahead of the line kernel
