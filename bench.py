@@ -296,10 +296,19 @@ def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
+    # one GPU per rank; with fewer GPUs than ranks (a functional check of the
+    # multi-rank path with --comm p2p on one device, not a scaling number)
+    # ranks share devices and the torch.distributed plumbing runs on gloo
+    ndev = max(1, torch.cuda.device_count())
+    shared = world > ndev
+    if shared and args.comm != "p2p":
+        raise SystemExit("more ranks than GPUs: only --comm p2p can share a device")
+    local = local % ndev
+    red_dev = "cpu" if shared else f"cuda:{local}"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group("gloo" if shared or not torch.cuda.is_available() else "nccl")
     torch.cuda.set_device(local)
     import paper_2109_04996_b200 as hx
     from paper_2109_04996_b200 import capi
@@ -365,7 +374,7 @@ def run_ours(args):
     barrier()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
+        t = torch.tensor([ms], device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -406,7 +415,7 @@ def run_ours(args):
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3) / args.steps
     assert all(r["iterations"] == args.iters for r in reps)
     if world > 1:
-        t = torch.tensor([e2e_ms, t_apply], device=f"cuda:{local}")
+        t = torch.tensor([e2e_ms, t_apply], device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms, t_apply = (float(v) for v in t.tolist())
     e2e_value = n_global * args.iters / (e2e_ms * 1e-3) / 1e9
@@ -427,7 +436,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     serial_ms = max(s0.elapsed_time(s1), (time.perf_counter() - w0) * 1e3) / serial_reps
     if world > 1:
-        t = torch.tensor([serial_ms], device=f"cuda:{local}")
+        t = torch.tensor([serial_ms], device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         serial_ms = float(t.item())
 
@@ -448,6 +457,8 @@ def run_ours(args):
                    "parallelism": (f"element partition {grid[0]}x{grid[1]}x{grid[2]} "
                                    f"(interface sum-exchange + all-reduce over "
                                    f"{'NVLink peer stores' if args.comm == 'p2p' else 'NCCL'})"
+                                   + (f"; {world} ranks sharing {ndev} GPU(s): a functional "
+                                      f"check, not a scaling number" if shared else "")
                                    if world > 1 else "single GPU"),
                    "l2_policy": "inputs larger than L2 (qdata 384 MB/GPU > 126 MB)"},
         "apply": {"gdofs": n_global / t_apply / 1e9, "us": t_apply * 1e6,
