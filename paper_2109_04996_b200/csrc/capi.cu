@@ -110,6 +110,17 @@ bool step_ap_zero() {
   return on;
 }
 
+// HXF_STEP_PDL=1: the operator kernel after a fused step kernel with
+// programmatic dependent launch (the step kernel triggers as each CTA ends).
+// Measured neutral to slightly worse (C3 CG 156.7 vs 157.4 us): kept off
+bool step_pdl() {
+  static const bool on = [] {
+    const char* v = std::getenv("HXF_STEP_PDL");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 bool dmma3_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("HXF_DMMA3");
@@ -338,7 +349,7 @@ bool k1_stores_cons(const hxf_op* op) {
 // constrained rows (no preset of them by the step kernel)
 void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double* dot_part,
                   int* nparts, const int* stop, bool zero_y = true, PcgState* st = nullptr,
-                  bool halo = true, int rev = 0, bool k1_cons = false) {
+                  bool halo = true, int rev = 0, bool k1_cons = false, bool k1_pdl = false) {
   // single-domain p = 7 collocated diffusion: y zeroed by a write-only memset
   // and the DMMA kernel stores y = x on the constrained rows it gathers
   // (instead of the read-x/write-y init_y pass)
@@ -351,7 +362,7 @@ void device_apply(hxf_op* op, const double* x, double* y, cudaStream_t s, double
   prm.cons_store = (cons_store || k1_cons) ? 1 : 0;
   // single apply: the kernel's factor copy and setup overlap the memset's tail
   // (it waits in griddepcontrol.wait before touching y); measured 90.6 -> 88.4 us
-  prm.pdl = cons_store && !pdl_apply_disabled() ? 1 : 0;
+  prm.pdl = (cons_store && !pdl_apply_disabled()) || (k1_pdl && step_pdl()) ? 1 : 0;
   prm.x = x;
   prm.y = y;
   prm.E = op->E;
@@ -550,7 +561,7 @@ void pcg_enqueue_iteration(const PcgSolve& ps, int it, cudaStream_t s, bool capt
   // partitioned: the interface sum-exchange of Ap is part of the apply
   // (overlapped with the interior elements where the kernel allows)
   device_apply(op, p, Ap, s, op->d_part, &nparts, &op->d_state->stop, /*zero_y=*/false,
-               op->d_state, /*halo=*/true, serp & (odd ^ 1), k1c);
+               op->d_state, /*halo=*/true, serp & (odd ^ 1), k1c, /*k1_pdl=*/fused && it > 1);
   if (ps.timed) record(op->ev[2 * (it - 1) + 1]);  // apply time (single GPU: K1 alone)
   if (fused) {
     ck(pcg_launch_step(s, op->d_state, it, op->w_hist.p, op->n_L, op->m, ps.dinv, r, ps.dx, p,

@@ -139,6 +139,7 @@ bool step_ap_zero();
 // HXF_DMMA3=0: BP6 p = 6, 7 on the component-by-component DMMA kernel instead
 // of the component-batched one (op_dmma3.cuh)
 bool dmma3_enabled();
+bool step_pdl();
 bool pdl_apply_disabled();    // HXF_PDL_APPLY=0: single apply without PDL (A/B)     // HXF_DMMA_PAD=0: p = 4..6 back on the pencil kernel (A/B)
 bool pdl_enabled();           // HXF_PDL=1: programmatic dependent launch (off by default)
 bool serpentine();            // HXF_SERPENTINE=0: all sweeps forward

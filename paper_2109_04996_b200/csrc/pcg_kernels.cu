@@ -579,6 +579,10 @@ __global__ void __launch_bounds__(ST_NT, 1)
     }
   }
   if (ts) g_step_ts[3][blockIdx.x] = gtimer();
+  // this CTA's vector writes are done: the next operator kernel may launch
+  // onto the SMs freed by the CTAs that finish first (it issues its first
+  // factor copy and waits in griddepcontrol.wait for this grid to complete)
+  pdl_trigger();
   const double sc = block_sum<ST_NT>(cc, scratch);
   if (threadIdx.x == 0) part[2 * G + blockIdx.x] = sc;
   if (!pcg_last_cta(&st->counter[2])) return;
