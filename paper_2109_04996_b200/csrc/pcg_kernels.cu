@@ -405,7 +405,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
 // runs instead of being flushed under the next operator kernel)
 // ST_U / ST_U2: grid-stride steps per loop trip of phase 1 / 2 (loads of all
 // of them first: phase 2 of an odd iteration has one global load per step)
-template <int ST_U, int ST_U2, bool ST_CS>
+template <int ST_U, int ST_U2, int ST_CS>
 __global__ void __launch_bounds__(ST_NT, 1)
     pcg_step_kernel(PcgState* st, int it, double* hist, int64_t n_L, int m,
                     const double* __restrict__ d, double* __restrict__ r, double* __restrict__ x,
@@ -569,11 +569,14 @@ __global__ void __launch_bounds__(ST_NT, 1)
       double2 pn;
       pn.x = z[u].x + beta * pv[u].x;
       pn.y = z[u].y + beta * pv[u].y;
-      po2[k[u]] = pn;
+      if (ST_CS >= 2) __stcs(po2 + k[u], pn); else po2[k[u]] = pn;
       int64_t node = 2 * (int64_t)k[u];
       if (m > 1) node -= (node / n_L) * n_L;
       const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
-      if (!ap_zero) a2[k[u]] = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
+      if (!ap_zero) {
+        const double2 av = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
+        if (ST_CS >= 3) __stcs(a2 + k[u], av); else a2[k[u]] = av;
+      }
       if (w & 1u) cc += pn.x * pn.x;
       if (w & 2u) cc += pn.y * pn.y;
     }
@@ -719,11 +722,16 @@ cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, 
                             double* part, int rev, int xmode, bool ap_zero) {
   // (measured, C3 CG iteration: phase 1 / 2 unrolled 1/2 158.6 us, 2/2 158.1,
   // 1/4 178.3 (spills) vs 1/1 156.8 — kept 1/1)
-  static const bool cs = [] {  // measured: C3 CG iteration 156.7 -> 155.9 us
+  // evict-first stores: 0 none, 1 x and r (measured: C3 CG iteration 156.7 ->
+  // 155.9 us), 2 + p, 3 + the Ap preset
+  static const int cs = [] {
     const char* v = std::getenv("HXF_STEP_CS");
-    return !(v && v[0] == '0');
+    return v ? std::atoi(v) : 1;
   }();
-  auto kern = cs ? pcg_step_kernel<1, 1, true> : pcg_step_kernel<1, 1, false>;
+  auto kern = cs == 0   ? pcg_step_kernel<1, 1, 0>
+              : cs == 2 ? pcg_step_kernel<1, 1, 2>
+              : cs == 3 ? pcg_step_kernel<1, 1, 3>
+                        : pcg_step_kernel<1, 1, 1>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ST_SMEM);
   if (attr != cudaSuccess) return attr;
