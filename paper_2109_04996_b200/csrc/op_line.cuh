@@ -111,8 +111,12 @@ struct LineTraits {
   // (measured, K1 at 1e7 DOFs: BP5 p = 4, 5, 6, 8 -13..14 %, BP3 p = 3, 4, 5, 7
   // -2..5 %; q <= 4 and BP3 p = 6 lose 2..8 % and keep the global loads)
   // (mass: interpolating bases only, where a barrier follows the QFunction)
+  // (collocated q = 11 stages its 64 KB too: measured BP5 p = 10 264 -> 239 us,
+  // BP6 p = 10 289 -> 270 us; with a 112 KB limit everywhere BP5 p = 9 / 11 and
+  // BP3 p = 8, 10, 11 lose 5..34 %)
   static constexpr bool QS = (DIFF || INTERP_) && Q >= 5 && !(INTERP_ && Q == 8) &&
-                             EPB * QDS * 8 <= (NC == 3 ? HXF_LINE_QSMEM_MAXKB3 : HXF_LINE_QSMEM_MAXKB) * 1024;
+                             (EPB * QDS * 8 <= (NC == 3 ? HXF_LINE_QSMEM_MAXKB3 : HXF_LINE_QSMEM_MAXKB) * 1024 ||
+                              (DIFF && !INTERP_ && Q == 11));
   static constexpr int OFF_QS = round_up(OFF_S + EPB * 3 * SLAB, 2);
   static constexpr int SMEM_BYTES = (OFF_QS + (QS ? EPB * QDS : 0)) * 8;
   __device__ static __forceinline__ int off(int k, int j, int i) { return (k * Q + j) * RS + i; }
