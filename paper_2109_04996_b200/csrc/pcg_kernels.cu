@@ -531,54 +531,81 @@ __global__ void __launch_bounds__(ST_NT, 1)
   const double2* pp2 = reinterpret_cast<const double2*>(xmode == 2 ? pprev : p);
   double2* po2 = reinterpret_cast<double2*>(pout);
   double cc = 0.0;
-  for (int j0 = nj - 1; j0 >= 0; j0 -= ST_U2) {
-    int k[ST_U2];
-    double2 pv[ST_U2], xv[ST_U2], qv[ST_U2], z[ST_U2];
-#pragma unroll
-    for (int u = 0; u < ST_U2; ++u) {
-      const int j = j0 - u;
-      k[u] = j >= 0 ? pair_at(j) : -1;
-      if (k[u] < 0) continue;
-      pv[u] = p2[k[u]];
-      if (xupd) xv[u] = x2[k[u]];
-      if (xupd && xmode == 2) qv[u] = pp2[k[u]];
-      const int q = j * ST_NT + (int)threadIdx.x;
-      if (!stop) {
-        if (q < zcap) {
-          z[u] = zc[q];
-        } else {
-          const double2 rv = r2[k[u]], dv = d ? d2[k[u]] : one2;
-          z[u] = make_double2(rv.x * dv.x, rv.y * dv.y);
-        }
+  // one direction step: x update (xmode), p = z + beta p, Ap preset, cc
+  auto dir_step = [&](int j, int kk, double2 pv, double2 xv, double2 qv) {
+    if (xupd) {
+      double2 xn = xv;
+      if (xmode == 2) {
+        xn.x = fma(alpha_prev, qv.x, xn.x);
+        xn.y = fma(alpha_prev, qv.y, xn.y);
       }
+      xn.x = fma(alpha, pv.x, xn.x);
+      xn.y = fma(alpha, pv.y, xn.y);
+      if (ST_CS) __stcs(x2 + kk, xn); else x2[kk] = xn;
     }
+    if (stop) return;
+    const int q = j * ST_NT + (int)threadIdx.x;
+    double2 z;
+    if (q < zcap) {
+      z = zc[q];
+    } else {
+      const double2 rv = r2[kk], dv = d ? d2[kk] : one2;
+      z = make_double2(rv.x * dv.x, rv.y * dv.y);
+    }
+    double2 pn;
+    pn.x = z.x + beta * pv.x;
+    pn.y = z.y + beta * pv.y;
+    if (ST_CS >= 2) __stcs(po2 + kk, pn); else po2[kk] = pn;
+    int64_t node = 2 * (int64_t)kk;
+    if (m > 1) node -= (node / n_L) * n_L;
+    const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
+    if (!ap_zero) {
+      const double2 av = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
+      if (ST_CS >= 3) __stcs(a2 + kk, av); else a2[kk] = av;
+    }
+    if (w & 1u) cc += pn.x * pn.x;
+    if (w & 2u) cc += pn.y * pn.y;
+  };
+  if constexpr (ST_U2 == 0) {
+    // the next step's p (and x, p_prev) loaded before this step is processed
+    const double2 zero2 = make_double2(0.0, 0.0);
+    int kc = pair_at(nj - 1);
+    double2 pc = zero2, xc = zero2, qc = zero2;
+    if (kc >= 0) {
+      pc = p2[kc];
+      if (xupd) xc = x2[kc];
+      if (xupd && xmode == 2) qc = pp2[kc];
+    }
+    for (int j = nj - 1; j >= 0; --j) {
+      const int kn = j > 0 ? pair_at(j - 1) : -1;
+      double2 pn_ = zero2, xn_ = zero2, qn_ = zero2;
+      if (kn >= 0) {
+        pn_ = p2[kn];
+        if (xupd) xn_ = x2[kn];
+        if (xupd && xmode == 2) qn_ = pp2[kn];
+      }
+      if (kc >= 0) dir_step(j, kc, pc, xc, qc);
+      kc = kn;
+      pc = pn_;
+      xc = xn_;
+      qc = qn_;
+    }
+  } else {
+    for (int j0 = nj - 1; j0 >= 0; j0 -= ST_U2) {
+      int k[ST_U2];
+      double2 pv[ST_U2], xv[ST_U2], qv[ST_U2];
 #pragma unroll
-    for (int u = 0; u < ST_U2; ++u) {
-      if (k[u] < 0) continue;
-      if (xupd) {
-        double2 xn = xv[u];
-        if (xmode == 2) {
-          xn.x = fma(alpha_prev, qv[u].x, xn.x);
-          xn.y = fma(alpha_prev, qv[u].y, xn.y);
-        }
-        xn.x = fma(alpha, pv[u].x, xn.x);
-        xn.y = fma(alpha, pv[u].y, xn.y);
-        if (ST_CS) __stcs(x2 + k[u], xn); else x2[k[u]] = xn;
+      for (int u = 0; u < ST_U2; ++u) {
+        const int j = j0 - u;
+        k[u] = j >= 0 ? pair_at(j) : -1;
+        if (k[u] < 0) continue;
+        pv[u] = p2[k[u]];
+        xv[u] = xupd ? x2[k[u]] : pv[u];
+        qv[u] = (xupd && xmode == 2) ? pp2[k[u]] : pv[u];
       }
-      if (stop) continue;
-      double2 pn;
-      pn.x = z[u].x + beta * pv[u].x;
-      pn.y = z[u].y + beta * pv[u].y;
-      if (ST_CS >= 2) __stcs(po2 + k[u], pn); else po2[k[u]] = pn;
-      int64_t node = 2 * (int64_t)k[u];
-      if (m > 1) node -= (node / n_L) * n_L;
-      const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
-      if (!ap_zero) {
-        const double2 av = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
-        if (ST_CS >= 3) __stcs(a2 + k[u], av); else a2[k[u]] = av;
-      }
-      if (w & 1u) cc += pn.x * pn.x;
-      if (w & 2u) cc += pn.y * pn.y;
+#pragma unroll
+      for (int u = 0; u < ST_U2; ++u)
+        if (k[u] >= 0) dir_step(j0 - u, k[u], pv[u], xv[u], qv[u]);
     }
   }
   if (ts) g_step_ts[3][blockIdx.x] = gtimer();
@@ -728,7 +755,12 @@ cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, 
     const char* v = std::getenv("HXF_STEP_CS");
     return v ? std::atoi(v) : 1;
   }();
-  auto kern = cs == 0   ? pcg_step_kernel<1, 1, 0>
+  static const bool pf = [] {  // HXF_STEP_PF=0: phase 2 without the one-step-ahead loads
+    const char* v = std::getenv("HXF_STEP_PF");
+    return !(v && v[0] == '0');
+  }();
+  auto kern = pf        ? pcg_step_kernel<1, 0, 1>
+              : cs == 0 ? pcg_step_kernel<1, 1, 0>
               : cs == 2 ? pcg_step_kernel<1, 1, 2>
               : cs == 3 ? pcg_step_kernel<1, 1, 3>
                         : pcg_step_kernel<1, 1, 1>;
