@@ -35,11 +35,16 @@ CASES = [
     ("bp6", 7, (6, 3, 3), "sine", 2),
     ("bp5", 7, (4, 4, 4), "none", 8),
     # three-component collocated kernels with the element list too: the pencil
-    # kernel (p = 1, 2, 5, 8, 9) and the zero-padded DMMA tile (p = 6)
+    # kernel (p = 1, 2, 5, 8, 9) and the component-batched DMMA kernel (p = 6, 7)
     ("bp6", 5, (4, 3, 3), "sine", 2),
     ("bp6", 8, (4, 2, 2), "sine", 2),
     ("bp6", 1, (6, 4, 4), "sine", 8),
     ("bp6", 6, (4, 4, 2), "sine", 4),
+    # high orders on the even-odd tensor-core kernel (element lists, staged /
+    # L2 factors, one and three components)
+    ("bp5", 13, (2, 2, 1), "sine", 2),
+    ("bp5", 15, (2, 1, 2), "sine", 2),
+    ("bp6", 12, (2, 2, 2), "sine", 4),
 ]
 
 
