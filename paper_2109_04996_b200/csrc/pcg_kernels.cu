@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(ST_NT, 1)
     pn.y = z.y + beta * pv.y;
     if (ST_CS >= 2) __stcs(po2 + kk, pn); else po2[kk] = pn;
     int64_t node = 2 * (int64_t)kk;
-    if (m > 1) node -= (node / n_L) * n_L;
+    for (int c = 1; c < m && node >= n_L; ++c) node -= n_L;  // component offset (no division)
     const uint32_t w = cons_mask ? (cons_mask[node >> 5] >> (node & 31)) & 3u : 0u;
     if (!ap_zero) {
       const double2 av = make_double2((w & 1u) ? pn.x : 0.0, (w & 2u) ? pn.y : 0.0);
