@@ -54,6 +54,13 @@ int64_t hxf_launch_count(void);
  * full-size configurations run.  Returns the previous cap.  Affects launches
  * made (and graphs captured) after the call. */
 int hxf_debug_set_grid_cap(int cap);
+/* Test knob: operator-kernel family for the collocated fast paths (0: the
+ * tuned dispatch — tensor-core kernels where available; 1: the register-line /
+ * pencil kernels instead of the tensor-core ones; 2: the general kernel
+ * op_apply_kernel everywhere, the A/B baseline and the path of bases that are
+ * not centro-symmetric).  Initial value from HXF_OP_KERNEL; returns the
+ * previous choice; affects launches made (and graphs captured) after the call. */
+int hxf_debug_set_op_kernel(int choice);
 /* Measurement knob: `on` != 0 makes the fused PCG step kernel record per-CTA
  * %globaltimer stamps (start, phase-1 end, after the grid barrier, phase-2
  * end) of its following launches; `out` (4 x 1024 uint64, or NULL) receives

@@ -30,7 +30,7 @@ EXPORTS = (
     "hxf_comm_group_destroy", "hxf_comm_create_group", "hxf_comm_destroy", "hxf_comm_rank",
     "hxf_comm_size", "hxf_comm_allreduce_sum", "hxf_operator_set_partition",
     "hxf_operator_halo_sum", "hxf_pcg_host_batch", "hxf_debug_set_grid_cap",
-    "hxf_debug_step_timestamps",
+    "hxf_debug_step_timestamps", "hxf_debug_set_op_kernel",
     "hxf_elem_restriction_create", "hxf_elem_restriction_destroy",
     "hxf_elem_restriction_is_structured", "hxf_elem_restriction_apply",
     "hxf_elem_restriction_multiplicity", "hxf_elem_restriction_gather_scalar",
@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
     L.hxf_pcg_host_batch.argtypes = [P, I, P, P, C.POINTER(PcgOptions), P, P]
     L.hxf_debug_set_grid_cap.argtypes = [I]
     L.hxf_debug_step_timestamps.argtypes = [I, C.c_void_p]
+    L.hxf_debug_set_op_kernel.argtypes = [I]
     L.hxf_elem_restriction_create.argtypes = [P, I, I, I64, I64, P, P, C.POINTER(P)]
     L.hxf_elem_restriction_destroy.argtypes = [P]
     L.hxf_elem_restriction_is_structured.argtypes = [P]
@@ -157,6 +158,13 @@ def check(rc: int) -> None:
     if rc == HXF_ENUMERIC:
         raise HxfNumericError(rc, msg)
     raise HxfError(rc, msg)
+
+
+def set_op_kernel(choice: int) -> int:
+    """Test knob (hxf_debug_set_op_kernel): 0 tuned dispatch, 1 line / pencil
+    kernels instead of the tensor-core ones, 2 the general kernel; returns the
+    previous choice."""
+    return int(lib().hxf_debug_set_op_kernel(int(choice)))
 
 
 def launch_count() -> int:

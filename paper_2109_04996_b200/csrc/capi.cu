@@ -72,15 +72,15 @@ int ablate_bits() {
   return bits;
 }
 
-int op_kernel_choice() {
-  static const int choice = [] {
-    const char* v = std::getenv("HXF_OP_KERNEL");
-    if (!v) return 0;
-    const std::string s(v);
-    return s == "pencil" ? 1 : (s == "generic" ? 2 : 0);
-  }();
-  return choice;
-}
+// HXF_OP_KERNEL (initial value) / hxf_debug_set_op_kernel
+std::atomic<int> g_op_choice{[] {
+  const char* v = std::getenv("HXF_OP_KERNEL");
+  if (!v) return 0;
+  const std::string s(v);
+  return s == "pencil" ? 1 : (s == "generic" ? 2 : 0);
+}()};
+
+int op_kernel_choice() { return g_op_choice.load(std::memory_order_relaxed); }
 
 bool pencil_disabled() {
   // HXF_PENCIL=0: collocated sizes without a tensor-core path on the line kernel (A/B)
@@ -694,6 +694,10 @@ int hxf_debug_set_grid_cap(int cap) {
   const int old = g_grid_cap.load();
   g_grid_cap.store(cap > 0 ? cap : 0);
   return old;
+}
+
+int hxf_debug_set_op_kernel(int choice) {
+  return g_op_choice.exchange(choice == 1 || choice == 2 ? choice : 0);
 }
 
 int hxf_debug_step_timestamps(int on, unsigned long long* out) {

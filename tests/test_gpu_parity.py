@@ -292,3 +292,34 @@ def test_pcg_history_multi_element_per_cta(ctx, grid_cap, cap, bp, p, dims):
     assert rep["iterations"] == rrep["iterations"] == 20
     assert oracle.rel_max_diff(rrep["residual_history"], rep["residual_history"]) <= 1e-10
     assert oracle.rel_max_diff(xr, x) <= 1e-10
+
+
+# ---- the other kernel families, forced (hxf_debug_set_op_kernel) ------------
+# 2: op_apply_kernel, the general kernel (A/B baseline; the path of bases that
+# are not centro-symmetric) for every BP; 1: the line / pencil kernels where
+# the tuned dispatch takes a tensor-core kernel
+@pytest.fixture
+def op_kernel():
+    old = capi.set_op_kernel(0)
+    yield capi.set_op_kernel
+    capi.set_op_kernel(old)
+
+
+@pytest.mark.parametrize("choice,bp,p,dims", [
+    (2, "bp5", 7, (3, 2, 2)), (2, "bp5", 3, (3, 3, 2)), (2, "bp3", 4, (2, 2, 2)),
+    (2, "bp6", 5, (2, 2, 1)), (2, "bp1", 3, (3, 2, 2)), (2, "bp2", 2, (2, 2, 2)),
+    (2, "bp4", 3, (2, 2, 1)), (2, "bp5", 12, (1, 1, 2)), (2, "bp6", 7, (2, 1, 1)),
+    (1, "bp5", 7, (3, 2, 2)), (1, "bp6", 7, (2, 2, 1)), (1, "bp6", 6, (2, 2, 1)),
+    (1, "bp5", 14, (1, 1, 2))])
+def test_apply_forced_kernel_families(ctx, op_kernel, choice, bp, p, dims):
+    op_kernel(choice)
+    pr = oracle.setup(bp, p, dims, "sine")
+    op = op_from_oracle(ctx, pr)
+    x = oracle.seeded_uniform(pr.size, 5 + p)
+    y = op.apply(x)
+    assert oracle.rel_max_diff(pr.apply(x), y) <= APPLY_TOL
+    d = op.diagonal()
+    assert np.array_equal(d, pr.diagonal())
+    xs, rep = op.pcg(pr.rhs, d, tol=1e-8, fixed_iterations=4)
+    xr, rrep = pr.solve(tol=1e-8, fixed_iterations=4)
+    assert oracle.rel_max_diff(rrep["residual_history"], rep["residual_history"]) <= 1e-10
