@@ -750,7 +750,8 @@ cudaError_t pcg_launch_step(cudaStream_t s, PcgState* st, int it, double* hist, 
   // (measured, C3 CG iteration: phase 1 / 2 unrolled 1/2 158.6 us, 2/2 158.1,
   // 1/4 178.3 (spills) vs 1/1 156.8 — kept 1/1)
   // evict-first stores: 0 none, 1 x and r (measured: C3 CG iteration 156.7 ->
-  // 155.9 us), 2 + p, 3 + the Ap preset
+  // 155.9 us), 2 + p, 3 + the Ap preset (both slower; so are write-through
+  // st.global.wt stores of x and r: 153.7 -> 156.7 us)
   static const int cs = [] {
     const char* v = std::getenv("HXF_STEP_CS");
     return v ? std::atoi(v) : 1;
