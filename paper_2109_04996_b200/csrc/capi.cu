@@ -131,16 +131,16 @@ bool dmma3_enabled() {
 
 bool dmmaeo_enabled(int P, int ncomp) {
   // measured (BP5 / BP6 ~1e7 DOFs, K1): the even-odd tensor-core kernel wins
-  // from p = 13 (one component: p = 13 294 vs 366 us, p = 15 201 vs 314 us;
-  // p = 12 311 vs 290) and p = 11 (three components: 321 vs 374 us, p = 15
-  // 195 vs 410 us); the line / pencil kernels stay ahead below
+  // from p = 12 (one component: p = 12 287 vs 289 us, p = 13 286 vs 366 us,
+  // p = 15 198 vs 314 us; p = 11 296 vs 261) and p = 11 (three components:
+  // 321 vs 374 us, p = 15 197 vs 410 us); the line / pencil kernels stay ahead below
   static const int mode = [] {
     const char* v = std::getenv("HXF_DMMAEO");
     return v ? std::atoi(v) : 1;
   }();
   if (mode == 0) return false;
   if (mode == 2) return true;  // every P = 9..16 (A/B)
-  return ncomp == 1 ? P >= 14 : P >= 12;
+  return ncomp == 1 ? P >= 13 : P >= 12;
 }
 
 bool dmma_pad_disabled() {

@@ -132,7 +132,7 @@ int op_kernel_choice();
 bool pencil_disabled();
 bool dmma_pad_disabled();
 // HXF_DMMAEO: even-odd tensor-core kernel for P = p+1 = 9..16 (op_dmmaeo.cuh):
-// unset / "1" where measured faster (P >= 14 one component, P >= 12 three),
+// unset / "1" where measured faster (P >= 13 one component, P >= 12 three),
 // "2" every P = 9..16, "0" off
 bool dmmaeo_enabled(int P, int ncomp);
 bool step_ap_zero();

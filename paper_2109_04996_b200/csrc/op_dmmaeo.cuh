@@ -81,6 +81,9 @@ struct EoTraits {
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ double2 ld_stream2(const double* p) {
@@ -275,30 +278,44 @@ __global__ void __launch_bounds__(T::NT, T::MINB) op_dmmaeo_kernel(const __grid_
             ((f & 16) && q.iz0 == 0) || ((f & 32) && q.iz0 + N - 1 == prm.NZ - 1);
     return q;
   };
+  // The element's x slab by rows: thread 2r + h copies half h (columns
+  // 8h .. min(N, 8h + 8)) of row r = (k, j) with cp.async, in 16-byte pairs
+  // when the global row is 16-byte aligned (the slab keeps (2m, 2m+1) pairs
+  // adjacent: the swizzle moves 4-double groups); and it masks those same
+  // points after its own copies landed.
+  // (measured: per-point copies with the index math per point cost ~12 % of
+  // the kernel's instructions at N = 14)
+  const bool gthr = tid < 2 * NN;
+  const int grow = tid >> 1, gk = grow / N, gj = grow - gk * N;
+  const int gc0 = (tid & 1) * 8, gc1 = gc0 + 8 < N ? gc0 + 8 : N;
+  const int ghx = 4 * (T::perm(gj & 3) ^ T::perm(gk & 3));
   auto issue_gather = [&](const Geo& q, int c, double* dst) {
-    if (prm.ablate & 1) return;  // measurement-only: no gather traffic
-    const double* src = prm.x + c * prm.n_L + q.base;
-    for (int n = tid; n < N3; n += NT) {
-      const int k = n / NN, rem = n - k * NN, j = rem / N, i = rem - j * N;
-      cp_async8(dst + T::off(k, j, i), src + i + prm.NX * j + NXY * k);
+    if ((prm.ablate & 1) || !gthr) return;
+    const double* g = prm.x + c * prm.n_L + q.base + prm.NX * gj + NXY * gk;
+    double* drow = dst + (gk * N + gj) * 16;
+    if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) {
+      int col = gc0;
+      for (; col + 1 < gc1; col += 2) cp_async16(drow + (col ^ ghx), g + col);
+      if (col < gc1) cp_async8(drow + (col ^ ghx), g + col);
+    } else {
+      for (int col = gc0; col < gc1; ++col) cp_async8(drow + (col ^ ghx), g + col);
     }
   };
   // own points of the gather: zero the constrained ones (y = x stored first
   // for a single apply that zero-filled y)
   auto mask_gather = [&](const Geo& q, int c, double* dst) {
-    if (!q.bnd) return;
+    if (!q.bnd || !gthr) return;
     const int f = prm.bnd_faces;
-    for (int n = tid; n < N3; n += NT) {
-      const int k = n / NN, rem = n - k * NN, j = rem / N, i = rem - j * N;
-      const int64_t ix = q.ix0 + i, iy = q.iy0 + j, iz = q.iz0 + k;
-      const bool cons = ((f & 1) && ix == 0) || ((f & 2) && ix == prm.NX - 1) ||
-                        ((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1) ||
-                        ((f & 16) && iz == 0) || ((f & 32) && iz == prm.NZ - 1);
-      if (cons) {
-        double* p = dst + T::off(k, j, i);
-        if (prm.cons_store) prm.y[c * prm.n_L + q.base + i + prm.NX * j + NXY * k] = *p;
-        *p = 0.0;
-      }
+    const int64_t iy = q.iy0 + gj, iz = q.iz0 + gk;
+    const bool row_all = ((f & 4) && iy == 0) || ((f & 8) && iy == prm.NY - 1) ||
+                         ((f & 16) && iz == 0) || ((f & 32) && iz == prm.NZ - 1);
+    const bool lo = (f & 1) && q.ix0 == 0, hi = (f & 2) && q.ix0 + N - 1 == prm.NX - 1;
+    double* drow = dst + (gk * N + gj) * 16;
+    for (int col = gc0; col < gc1; ++col) {
+      if (!(row_all || (col == 0 && lo) || (col == N - 1 && hi))) continue;
+      double* p = drow + (col ^ ghx);
+      if (prm.cons_store) prm.y[c * prm.n_L + q.base + col + prm.NX * gj + NXY * gk] = *p;
+      *p = 0.0;
     }
   };
 

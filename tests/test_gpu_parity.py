@@ -194,7 +194,7 @@ def test_apply_vs_oracle_across_orders(ctx, bp, p, dims):
     assert oracle.rel_max_diff(pr.apply(x), op.apply(x)) <= APPLY_TOL
 
 
-# even-odd FP64 tensor-core kernel (op_dmmaeo.cuh; dispatched for p >= 13 one
+# even-odd FP64 tensor-core kernel (op_dmmaeo.cuh; dispatched for p >= 12 one
 # component, p >= 11 three): odd and even N = p+1, factors staged in shared
 # memory (N <= 14) or read from L2 (N = 15, 16), box-constrained sine meshes;
 # the lower orders of the list run the line / pencil kernels
