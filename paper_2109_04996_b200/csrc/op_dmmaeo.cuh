@@ -63,6 +63,8 @@ struct EoTraits {
   // QS: the element's factors staged in shared memory by bulk copies (TMA
   // engine), issued as soon as the previous element's QFunction consumed
   // them; N = 15, 16 do not fit (162 / 196 KB) and read them from L2 instead
+  // (measured and dropped for N = 16: staging the first 8 rows of every factor
+  // plane with 96 bulk copies per element, BP5 p = 15 198 -> 235 us)
   static constexpr int SLABS_BYTES = 3 * SLAB * 8;
   static constexpr bool QS = SLABS_BYTES + QDS * 8 + 4096 <= 227 * 1024;
   static constexpr int SMEM_BYTES = SLABS_BYTES + (QS ? QDS * 8 : 0);
